@@ -1,0 +1,88 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel
+to the GPU box with the repo snapshot).
+
+  libllsa_cuda.so   every CUDA kernel + the C ABI (include/llsa_cuda.h),
+                    compiled for sm_100a only
+  libllsa.so        the C++ operator API mirroring the reference
+                    (include/llsa/*.hpp), on top of libllsa_cuda.so
+
+Incremental: an object is rebuilt when its source or any header is newer.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "lib")
+OBJ = os.path.join(PKG, "build", "obj")
+INCLUDE = os.path.join(ROOT, "include")
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+CXX = shutil.which("g++") or "g++"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                     "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
+                     f"-I{INCLUDE}", f"-I{CSRC}"]
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", f"-I{INCLUDE}",
+             "-I/usr/local/cuda/include"]
+
+CUDA_LIB = os.path.join(OUT, "libllsa_cuda.so")
+SHIM_LIB = os.path.join(OUT, "libllsa.so")
+
+
+def _headers() -> list[str]:
+    hs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+    hs += glob.glob(os.path.join(INCLUDE, "*.h")) + glob.glob(os.path.join(INCLUDE, "llsa", "*.hpp"))
+    return hs
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {cmd[-1]}")
+
+
+def build(verbose: bool = False, force: bool = False) -> dict[str, str]:
+    os.makedirs(OUT, exist_ok=True)
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = _headers()
+    cu = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    jobs = []
+    objs = []
+    for src in cu:
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + hdrs):
+            jobs.append([NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj])
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        for f in [ex.submit(_run, j) for j in jobs]:
+            f.result()
+    if force or jobs or _stale(CUDA_LIB, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB] + objs + ["-lcuda"])
+    shim_src = sorted(glob.glob(os.path.join(CSRC, "shim", "*.cpp")))
+    if shim_src and (force or _stale(SHIM_LIB, shim_src + hdrs + [CUDA_LIB])):
+        _run([CXX] + CXX_FLAGS + ["-shared", "-o", SHIM_LIB] + shim_src +
+             [f"-L{OUT}", "-lllsa_cuda", f"-Wl,-rpath,$ORIGIN",
+              "-L/usr/local/cuda/lib64", "-lcudart"])
+    if verbose:
+        print(f"built {CUDA_LIB}" + (f", {SHIM_LIB}" if shim_src else ""))
+    return {"cuda": CUDA_LIB, "shim": SHIM_LIB if shim_src else ""}
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)

@@ -1,0 +1,693 @@
+// The C ABI (include/llsa_cuda.h): argument/config validation in the
+// reference's order and error kinds, then stream-ordered kernel launches.
+// No entry point synchronises; device-detected errors land in a sticky
+// per-device flag read by llsa_sync_status().
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "internal.h"
+#include "tc.h"
+#include "common.cuh"
+
+namespace llsa_impl {
+
+namespace {
+thread_local char g_msg[512] = "";
+thread_local uint32_t g_launches = 0;
+std::mutex g_flag_mu;
+uint32_t* g_flags[64] = {};
+}  // namespace
+
+llsa_status fail(llsa_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_msg, sizeof(g_msg), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+llsa_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(LLSA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+void count_launch(uint32_t n) { g_launches += n; }
+uint32_t take_launch_count() {
+  const uint32_t n = g_launches;
+  g_launches = 0;
+  return n;
+}
+
+uint32_t* device_flag() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_flag_mu);
+  if (!g_flags[dev]) {
+    uint32_t* p = nullptr;
+    if (cudaMalloc(&p, sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, sizeof(uint32_t));
+    g_flags[dev] = p;
+  }
+  return g_flags[dev];
+}
+
+static uint32_t max_levels_impl(uint64_t n, uint32_t b) {
+  if (b < 2 || n == 0) return 0;  // config.cpp:54-64
+  uint32_t l = 0;
+  uint64_t p = b;
+  while (p <= n / b) {
+    p *= b;
+    ++l;
+  }
+  return l;
+}
+
+llsa_status make_geometry(const llsa_config* c, Geometry* g) {
+  if (!c) return fail(LLSA_ERR_ARGUMENT, "null config");
+  // validate_config, P/src/config.cpp:66-117 — same checks, same order.
+  if (c->n == 0) return fail(LLSA_ERR_CONFIG, "sequence length must be positive");
+  if (c->d == 0) return fail(LLSA_ERR_CONFIG, "feature dimension must be positive");
+  if (c->block_size < 2) return fail(LLSA_ERR_CONFIG, "block size must be at least 2");
+  if (c->n > 0xffffffffull)
+    return fail(LLSA_ERR_CONFIG, "sequence length exceeds the 32-bit index range");
+  if (!std::isfinite(c->softmax_scale) || c->softmax_scale < 0.f)
+    return fail(LLSA_ERR_CONFIG, "softmax scale must be finite and non-negative");
+  const uint32_t lmax = max_levels_impl(c->n, c->block_size);
+  if (c->levels < 1 || c->levels > lmax)
+    return fail(LLSA_ERR_LEVEL, "levels must lie in [1, %u] for n=%llu, block size %u", lmax,
+                (unsigned long long)c->n, c->block_size);
+  uint64_t pow_l = 1;
+  for (uint32_t l = 0; l < c->levels; ++l) pow_l *= c->block_size;
+  if (c->n % pow_l != 0)
+    return fail(LLSA_ERR_DIVISIBILITY,
+                "sequence length %llu is not divisible by block_size^levels = %llu",
+                (unsigned long long)c->n, (unsigned long long)pow_l);
+  if (c->enrich_levels > c->levels)
+    return fail(LLSA_ERR_LEVEL, "enrich_levels %u exceeds levels %u", c->enrich_levels,
+                c->levels);
+  const uint64_t coarsest = c->n / pow_l;
+  if (c->top_k < 1 || c->top_k > coarsest)
+    return fail(LLSA_ERR_TOPK, "top_k must lie in [1, %llu] (coarsest-level candidate count)",
+                (unsigned long long)coarsest);
+  if (c->reweight_mode > 1) return fail(LLSA_ERR_ARGUMENT, "bad reweight mode");
+
+  Geometry G;
+  G.n = c->n;
+  G.d = c->d;
+  G.B = c->block_size;
+  G.K = c->top_k;
+  G.L = c->levels;
+  G.Le = c->enrich_levels;
+  G.scale = c->softmax_scale > 0.f ? c->softmax_scale : 1.0f / std::sqrt((float)c->d);
+  G.mode = c->reweight_mode;
+  G.safe = c->safe_softmax ? 1 : 0;
+  G.pow[0] = 1;
+  for (uint32_t l = 1; l <= G.L + 1; ++l) G.pow[l] = G.pow[l - 1] * G.B;
+  G.pyr_rows = 0;
+  for (uint32_t l = 1; l <= G.L; ++l) {
+    G.pyr_off[l] = G.pyr_rows;
+    G.pyr_rows += G.n / G.pow[l];
+  }
+  G.table_entries = 0;
+  G.csc_off_entries = G.csc_flat_entries = 0;
+  for (uint32_t l = 0; l < G.L; ++l) {
+    G.table_off[l] = G.table_entries;
+    G.csc_off_off[l] = G.csc_off_entries;
+    G.csc_flat_off[l] = G.csc_flat_entries;
+    G.table_entries += G.level_blocks(l) * G.K;
+    G.csc_off_entries += G.level_blocks(l) + 1;
+    G.csc_flat_entries += G.level_blocks(l) * G.K;
+  }
+  // effective_block_count, config.cpp:119-125
+  G.E = G.K * G.enrich_lim() + (G.Le == G.L ? (uint32_t)G.level_blocks(G.L) : 0u);
+  *g = G;
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl
+
+using namespace llsa_impl;
+
+namespace {
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+#define NONNULL(p)                                                       \
+  do {                                                                   \
+    if (!(p)) return fail(LLSA_ERR_ARGUMENT, "null pointer: %s", #p);   \
+  } while (0)
+
+llsa_status dtype_ok(llsa_dtype dt) {
+  if (dt != LLSA_F32 && dt != LLSA_BF16) return fail(LLSA_ERR_ARGUMENT, "bad dtype %d", dt);
+  return LLSA_OK;
+}
+
+llsa_status hier_topk(const Geometry& g, uint32_t units, const float* pyr_q,
+                      const float* pyr_k, uint32_t* tables, cudaStream_t s) {
+  const uint64_t ps = g.pyr_rows * g.d;
+  const uint64_t top = g.level_tokens(g.L);
+  // coarsest stage on level L → table level L-1 (selection.cpp:167-169)
+  llsa_status st = launch_select_coarsest(
+      pyr_q + g.pyr_off[g.L] * g.d, ps, pyr_k + g.pyr_off[g.L] * g.d, ps, units,
+      (uint32_t)top, (uint32_t)top, g.d, g.K, g.scale, tables + g.table_off[g.L - 1],
+      g.table_entries, s);
+  if (st) return st;
+  for (uint32_t l = g.L - 1; l >= 1; --l) {  // selection.cpp:170-175
+    st = launch_select_level(pyr_q + g.pyr_off[l] * g.d, ps, pyr_k + g.pyr_off[l] * g.d, ps,
+                             tables + g.table_off[l], g.table_entries, units,
+                             (uint32_t)g.level_blocks(l), g.K, g.level_tokens(l), g.d, g.K,
+                             g.scale, g.B, tables + g.table_off[l - 1], g.table_entries, s);
+    if (st) return st;
+  }
+  return LLSA_OK;
+}
+
+llsa_status pyramid(const Geometry& g, uint32_t units, const void* x, llsa_dtype dt,
+                    float* out, cudaStream_t s) {
+  const uint64_t ps = g.pyr_rows * g.d;
+  llsa_status st = launch_pool_level(x, dt, g.n * g.d, out, ps, units, g.level_tokens(1), g.d,
+                                     g.B, s);
+  for (uint32_t l = 2; l <= g.L && st == LLSA_OK; ++l)
+    st = launch_pool_level(out + g.pyr_off[l - 1] * g.d, LLSA_F32, ps, out + g.pyr_off[l] * g.d,
+                           ps, units, g.level_tokens(l), g.d, g.B, s);
+  return st;
+}
+
+llsa_status transpose_all_impl(const Geometry& g, uint32_t units, const uint32_t* tables,
+                               uint32_t* offs, uint32_t* flat, void* ws, cudaStream_t s) {
+  for (uint32_t l = 0; l < g.L; ++l) {
+    const uint32_t kb = (uint32_t)g.level_blocks(l);
+    llsa_status st = launch_transpose(tables + g.table_off[l], g.table_entries, units, kb,
+                                      g.K, kb, offs + g.csc_off_off[l], g.csc_off_entries,
+                                      flat + g.csc_flat_off[l], g.csc_flat_entries, ws, s);
+    if (st) return st;
+  }
+  return LLSA_OK;
+}
+
+size_t transpose_all_ws(const Geometry& g, uint32_t units) {
+  size_t m = 256;
+  for (uint32_t l = 0; l < g.L; ++l) {
+    const uint32_t kb = (uint32_t)g.level_blocks(l);
+    const size_t b = transpose_ws_bytes(units, kb, g.K, kb);
+    if (b > m) m = b;
+  }
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+int llsa_abi_version(void) { return LLSA_CUDA_ABI_VERSION; }
+const char* llsa_last_error(void) { return g_msg; }
+
+const char* llsa_status_name(llsa_status s) {
+  switch (s) {
+    case LLSA_OK: return "ok";
+    case LLSA_ERR_CONFIG: return "ConfigError";
+    case LLSA_ERR_DIVISIBILITY: return "DivisibilityError";
+    case LLSA_ERR_LEVEL: return "LevelError";
+    case LLSA_ERR_TOPK: return "TopKError";
+    case LLSA_ERR_SHAPE: return "ShapeMismatch";
+    case LLSA_ERR_INDEX_RANGE: return "IndexOutOfRange";
+    case LLSA_ERR_NONFINITE: return "NonFiniteError";
+    case LLSA_ERR_STALE_STATE: return "StaleState";
+    case LLSA_ERR_FORMAT: return "FormatError";
+    case LLSA_ERR_IO: return "IoError";
+    case LLSA_ERR_PRECISION: return "PrecisionError";
+    case LLSA_ERR_NOT_SQUARE_BLOCK: return "NotSquareBlock";
+    case LLSA_ERR_ORACLE_CAP: return "OracleCapExceeded";
+    case LLSA_ERR_CUDA: return "CudaError";
+    case LLSA_ERR_UNSUPPORTED: return "Unsupported";
+    case LLSA_ERR_ARGUMENT: return "ArgumentError";
+  }
+  return "unknown";
+}
+
+llsa_status llsa_sync_status(void* stream) {
+  LLSA_CUDA_TRY(cudaStreamSynchronize(S(stream)));
+  uint32_t* f = device_flag();
+  if (!f) return fail(LLSA_ERR_CUDA, "no device flag");
+  uint32_t h = 0;
+  LLSA_CUDA_TRY(cudaMemcpy(&h, f, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h) LLSA_CUDA_TRY(cudaMemset(f, 0, sizeof(uint32_t)));
+  if (h & llsa_dev::kErrIndex)
+    return fail(LLSA_ERR_INDEX_RANGE, "selection or plan entry outside its level");
+  if (h & llsa_dev::kErrNonFinite)
+    return fail(LLSA_ERR_NONFINITE, "attention output contains non-finite values");
+  return LLSA_OK;
+}
+
+uint32_t llsa_max_levels(uint64_t n, uint32_t b) { return max_levels_impl(n, b); }
+
+llsa_status llsa_validate_config(const llsa_config* cfg, float* scale, uint32_t* eff) {
+  Geometry g;
+  llsa_status st = make_geometry(cfg, &g);
+  if (st) return st;
+  if (scale) *scale = g.scale;
+  if (eff) *eff = g.E;
+  return LLSA_OK;
+}
+
+uint64_t llsa_pyramid_rows(uint64_t n, uint32_t b, uint32_t levels) {
+  uint64_t r = 0, t = n;
+  for (uint32_t l = 1; l <= levels && b; ++l) {
+    t /= b;
+    r += t;
+  }
+  return r;
+}
+
+uint64_t llsa_table_entries(const llsa_config* cfg) {
+  Geometry g;
+  return make_geometry(cfg, &g) ? 0 : g.table_entries;
+}
+uint64_t llsa_csc_offsets_entries(const llsa_config* cfg) {
+  Geometry g;
+  return make_geometry(cfg, &g) ? 0 : g.csc_off_entries;
+}
+uint64_t llsa_csc_flat_entries(const llsa_config* cfg) {
+  Geometry g;
+  return make_geometry(cfg, &g) ? 0 : g.csc_flat_entries;
+}
+
+uint64_t llsa_select_mul_accs(const llsa_config* cfg) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  const uint64_t top = g.level_tokens(g.L);
+  uint64_t m = top * top * g.d;  // selection.cpp:75-77
+  for (uint32_t l = 1; l < g.L; ++l) m += g.level_tokens(l) * g.K * g.B * g.d;  // :145-147
+  return m;
+}
+
+uint64_t llsa_forward_mul_accs(const llsa_config* cfg) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  return g.n * g.E * g.B * g.d;  // attention.cpp:163
+}
+
+uint64_t llsa_backward_mul_accs(const llsa_config* cfg) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  // attention_grad.cpp:258-259 (dq + D) and :114,164,198 (kv incl. its own D)
+  uint64_t m = g.n * g.E * g.B * 3 * g.d + 2 * g.n * g.d;
+  uint64_t kv = 2 * g.n * g.d;
+  for (uint32_t l = 0; l < g.enrich_lim(); ++l)
+    kv += g.level_blocks(l) * g.K * g.pow[l + 1] * g.B * 4 * g.d;
+  if (g.Le == g.L) kv += g.n * g.level_tokens(g.L) * 4 * g.d;
+  return m + kv;
+}
+
+llsa_status llsa_build_pyramid(const void* x, llsa_dtype dt, uint32_t units, uint64_t rows,
+                               uint32_t d, uint32_t B, uint32_t levels, float* out,
+                               void* stream) {
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (B < 2) return fail(LLSA_ERR_DIVISIBILITY, "block size must be at least 2");
+  uint64_t r = rows;
+  for (uint32_t l = 1; l <= levels; ++l) {  // pyramid.cpp:23-28
+    if (r % B != 0)
+      return fail(LLSA_ERR_DIVISIBILITY, "level %u has %llu rows, not a multiple of block size %u",
+                  l - 1, (unsigned long long)r, B);
+    r /= B;
+  }
+  if (levels == 0 || units == 0 || rows == 0) return LLSA_OK;
+  NONNULL(x);
+  NONNULL(out);
+  const uint64_t pr = llsa_pyramid_rows(rows, B, levels);
+  llsa_status st = launch_pool_level(x, dt, rows * d, out, pr * d, units, rows / B, d, B,
+                                     S(stream));
+  uint64_t off_prev = 0, rows_prev = rows / B;
+  for (uint32_t l = 2; l <= levels && st == LLSA_OK; ++l) {
+    const uint64_t off = off_prev + rows_prev;
+    st = launch_pool_level(out + off_prev * d, LLSA_F32, pr * d, out + off * d, pr * d, units,
+                           rows_prev / B, d, B, S(stream));
+    off_prev = off;
+    rows_prev /= B;
+  }
+  return st;
+}
+
+llsa_status llsa_pool_backward(const float* g, uint32_t units, uint64_t coarse_rows, uint32_t d,
+                               uint32_t B, uint32_t hops, float* out, void* stream) {
+  const uint64_t group = llsa_dev::ipow_u64(B, hops);
+  if (hops == 0) {  // pyramid.cpp:47: identity
+    if (units && coarse_rows && d) {
+      NONNULL(g);
+      NONNULL(out);
+      LLSA_CUDA_TRY(cudaMemcpyAsync(out, g, (size_t)units * coarse_rows * d * 4,
+                                    cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    return LLSA_OK;
+  }
+  if (B < 2) return fail(LLSA_ERR_DIVISIBILITY, "block size must be at least 2");
+  if (units == 0 || coarse_rows == 0 || d == 0) return LLSA_OK;
+  NONNULL(g);
+  NONNULL(out);
+  return launch_pool_backward(g, units, coarse_rows, d, group, out, S(stream));
+}
+
+llsa_status llsa_select_coarsest(const float* q, const float* k, uint32_t units, uint32_t rows,
+                                 uint32_t cands, uint32_t d, uint32_t top_k, float scale,
+                                 uint32_t* out, void* stream) {
+  if (top_k < 1 || top_k > cands)  // selection.cpp:48-51
+    return fail(LLSA_ERR_TOPK, "top_k %u outside [1, %u]", top_k, cands);
+  if (units == 0 || rows == 0) return LLSA_OK;
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(out);
+  return launch_select_coarsest(q, (uint64_t)rows * d, k, (uint64_t)cands * d, units, rows,
+                                cands, d, top_k, scale, out, (uint64_t)rows * top_k, S(stream));
+}
+
+llsa_status llsa_select_level(const float* q, const float* k, const uint32_t* parent,
+                              uint32_t units, uint32_t parent_level, uint32_t parent_rows,
+                              uint32_t parent_k, uint64_t k_rows, uint32_t d, uint32_t top_k,
+                              float scale, uint32_t B, uint32_t* out, void* stream) {
+  // selection.cpp:84-105, same order
+  if (parent_level == 0)
+    return fail(LLSA_ERR_LEVEL, "select_level needs a parent table at level >= 1");
+  if (B == 0 || k_rows % B != 0)
+    return fail(LLSA_ERR_SHAPE, "level selection: key token count not a multiple of the "
+                "block size");
+  const uint64_t cand = (uint64_t)parent_k * B;
+  if (top_k < 1 || top_k > cand)
+    return fail(LLSA_ERR_TOPK, "top_k %u outside [1, %llu]", top_k, (unsigned long long)cand);
+  if (units == 0 || parent_rows == 0) return LLSA_OK;
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(parent);
+  NONNULL(out);
+  return launch_select_level(q, (uint64_t)parent_rows * B * d, k, k_rows * d, parent,
+                             (uint64_t)parent_rows * parent_k, units, parent_rows, parent_k,
+                             k_rows, d, top_k, scale, B, out,
+                             (uint64_t)parent_rows * B * top_k, S(stream));
+}
+
+llsa_status llsa_hierarchical_topk(const llsa_config* cfg, uint32_t units, const float* pyr_q,
+                                   const float* pyr_k, uint32_t* tables, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(pyr_q);
+  NONNULL(pyr_k);
+  NONNULL(tables);
+  return hier_topk(g, units, pyr_q, pyr_k, tables, S(stream));
+}
+
+size_t llsa_transpose_workspace_bytes(uint32_t units, uint32_t rows, uint32_t k,
+                                      uint32_t key_blocks) {
+  return transpose_ws_bytes(units, rows, k, key_blocks);
+}
+
+llsa_status llsa_transpose_indices(const uint32_t* idx, uint32_t units, uint32_t rows,
+                                   uint32_t k, uint32_t key_blocks, uint32_t* offsets,
+                                   uint32_t* flat, void* ws, size_t ws_bytes, void* stream) {
+  if (units == 0) return LLSA_OK;
+  NONNULL(offsets);
+  if ((uint64_t)rows * k) {
+    NONNULL(idx);
+    NONNULL(flat);
+  }
+  if (!ws || ws_bytes < transpose_ws_bytes(units, rows, k, key_blocks))
+    return fail(LLSA_ERR_ARGUMENT, "transpose workspace too small");
+  return launch_transpose(idx, (uint64_t)rows * k, units, rows, k, key_blocks, offsets,
+                          (uint64_t)key_blocks + 1, flat, (uint64_t)rows * k, ws, S(stream));
+}
+
+size_t llsa_transpose_all_workspace_bytes(const llsa_config* cfg, uint32_t units) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  return transpose_all_ws(g, units);
+}
+
+llsa_status llsa_transpose_all(const llsa_config* cfg, uint32_t units, const uint32_t* tables,
+                               uint32_t* offs, uint32_t* flat, void* ws, size_t ws_bytes,
+                               void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(tables);
+  NONNULL(offs);
+  NONNULL(flat);
+  if (!ws || ws_bytes < transpose_all_ws(g, units))
+    return fail(LLSA_ERR_ARGUMENT, "transpose workspace too small");
+  return transpose_all_impl(g, units, tables, offs, flat, ws, S(stream));
+}
+
+llsa_status llsa_build_plan(const llsa_config* cfg, uint32_t units, const uint32_t* tables,
+                            uint32_t* pl, uint32_t* pb, float* pw, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(tables);
+  NONNULL(pl);
+  NONNULL(pb);
+  NONNULL(pw);
+  return launch_build_plan(g, units, tables, pl, pb, pw, S(stream));
+}
+
+llsa_status llsa_forward(const llsa_config* cfg, uint32_t units, llsa_dtype dt, const void* q,
+                         const void* k, const void* v, const float* pyr_k, const float* pyr_v,
+                         const uint32_t* tables, float* out, float* rm, float* rd,
+                         void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(tables);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  if (g.L >= 1 && (!pyr_k || !pyr_v)) return fail(LLSA_ERR_ARGUMENT, "null pyramid");
+  return simt_forward(g, units, dt, q, k, v, pyr_k, pyr_v, tables, out, rm, rd, S(stream));
+}
+
+size_t llsa_backward_workspace_bytes(const llsa_config* cfg, uint32_t units) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  return simt_backward_ws_bytes(g, units);
+}
+
+llsa_status llsa_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                          const void* d_out, const float* out, const float* rm,
+                          const float* rd, const void* q, const void* k, const void* v,
+                          const float* pyr_k, const float* pyr_v, const uint32_t* tables,
+                          const uint32_t* offs, const uint32_t* flat, float* dq, float* dk,
+                          float* dv, void* ws, size_t ws_bytes, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(d_out);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(pyr_k);
+  NONNULL(pyr_v);
+  NONNULL(tables);
+  NONNULL(offs);
+  NONNULL(flat);
+  NONNULL(dq);
+  NONNULL(dk);
+  NONNULL(dv);
+  if (!ws || ws_bytes < simt_backward_ws_bytes(g, units))
+    return fail(LLSA_ERR_ARGUMENT, "backward workspace too small");
+  return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, tables, offs,
+                       flat, dq, dk, dv, ws, S(stream));
+}
+
+llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                             const void* d_out, const float* out, const float* rm,
+                             const float* rd, const void* q, const float* pyr_k,
+                             const float* pyr_v, const void* k, const void* v,
+                             const uint32_t* offs, const uint32_t* flat, float* dk, float* dv,
+                             void* ws, size_t ws_bytes, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(d_out);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(pyr_k);
+  NONNULL(pyr_v);
+  NONNULL(offs);
+  NONNULL(flat);
+  NONNULL(dk);
+  NONNULL(dv);
+  if (!ws || ws_bytes < simt_backward_ws_bytes(g, units))
+    return fail(LLSA_ERR_ARGUMENT, "backward workspace too small");
+  return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, nullptr, offs,
+                       flat, nullptr, dk, dv, ws, S(stream));
+}
+
+// ---------------------------------------------------------------------------
+// Handle (fused) API
+// ---------------------------------------------------------------------------
+struct llsa_handle_s {
+  Geometry g;
+  uint32_t units = 0;
+  llsa_dtype dt = LLSA_BF16;
+  bool tc = false;
+  int device = 0;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  float *pyr_q = nullptr, *pyr_k = nullptr, *pyr_v = nullptr;
+  uint32_t *tables = nullptr, *csc_off = nullptr, *csc_flat = nullptr;
+  float *row_max = nullptr, *row_denom = nullptr;
+  void* tr_ws = nullptr;
+  size_t tr_ws_bytes = 0;
+  void* bwd_ws = nullptr;
+  size_t bwd_ws_bytes = 0;
+  TcBuffers tcb;
+  uint32_t last_launches = 0;
+  size_t sizes[8] = {};
+};
+
+llsa_status llsa_handle_create(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                               llsa_handle* out) {
+  NONNULL(out);
+  *out = nullptr;
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return fail(LLSA_ERR_ARGUMENT, "units must be positive");
+  auto* h = new (std::nothrow) llsa_handle_s();
+  if (!h) return fail(LLSA_ERR_CUDA, "out of host memory");
+  h->g = g;
+  h->units = units;
+  h->dt = dt;
+  h->tc = tc_supported(g, dt);
+  cudaGetDevice(&h->device);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t pyr = al((size_t)units * g.pyr_rows * g.d * 4);
+  const size_t tab = al((size_t)units * g.table_entries * 4);
+  const size_t coff = al((size_t)units * g.csc_off_entries * 4);
+  const size_t cflat = al((size_t)units * g.csc_flat_entries * 4);
+  const size_t rows = al((size_t)units * g.n * 4);
+  h->tr_ws_bytes = al(transpose_all_ws(g, units));
+  h->bwd_ws_bytes = al(h->tc ? tc_backward_ws_bytes(g, units) : simt_backward_ws_bytes(g, units));
+  const size_t tcb = h->tc ? al(tc_buffer_bytes(g, units)) : 0;
+  h->arena_bytes = 3 * pyr + tab + coff + cflat + 2 * rows + h->tr_ws_bytes + h->bwd_ws_bytes +
+                   tcb + 256;
+  if (cudaMalloc(&h->arena, h->arena_bytes) != cudaSuccess) {
+    delete h;
+    return fail(LLSA_ERR_CUDA, "cudaMalloc of %zu bytes failed", (size_t)0);
+  }
+  char* p = h->arena;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += b;
+    return r;
+  };
+  h->pyr_q = reinterpret_cast<float*>(take(pyr));
+  h->pyr_k = reinterpret_cast<float*>(take(pyr));
+  h->pyr_v = reinterpret_cast<float*>(take(pyr));
+  h->tables = reinterpret_cast<uint32_t*>(take(tab));
+  h->csc_off = reinterpret_cast<uint32_t*>(take(coff));
+  h->csc_flat = reinterpret_cast<uint32_t*>(take(cflat));
+  h->row_max = reinterpret_cast<float*>(take(rows));
+  h->row_denom = reinterpret_cast<float*>(take(rows));
+  h->tr_ws = take(h->tr_ws_bytes);
+  h->bwd_ws = take(h->bwd_ws_bytes);
+  if (h->tc) tc_carve(g, units, take(tcb), &h->tcb);
+  const size_t sz[8] = {pyr, pyr, pyr, tab, coff, cflat, rows, rows};
+  memcpy(h->sizes, sz, sizeof(sz));
+  *out = h;
+  return LLSA_OK;
+}
+
+llsa_status llsa_handle_destroy(llsa_handle h) {
+  if (!h) return LLSA_OK;
+  if (h->arena) cudaFree(h->arena);
+  delete h;
+  return LLSA_OK;
+}
+
+int llsa_handle_uses_tensor_cores(llsa_handle h) { return h && h->tc ? 1 : 0; }
+
+llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, const void* v,
+                                float* out, void* stream) {
+  NONNULL(h);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(out);
+  const Geometry& g = h->g;
+  cudaStream_t s = S(stream);
+  take_launch_count();
+  llsa_status st = pyramid(g, h->units, q, h->dt, h->pyr_q, s);
+  if (!st) st = pyramid(g, h->units, k, h->dt, h->pyr_k, s);
+  if (!st) st = pyramid(g, h->units, v, h->dt, h->pyr_v, s);
+  if (!st) st = hier_topk(g, h->units, h->pyr_q, h->pyr_k, h->tables, s);
+  if (!st) {
+    if (h->tc)
+      st = tc_forward(g, h->units, q, k, v, h->pyr_k, h->pyr_v, h->tables, out, h->row_max,
+                      h->row_denom, h->tcb, s);
+    else
+      st = simt_forward(g, h->units, h->dt, q, k, v, h->pyr_k, h->pyr_v, h->tables, out,
+                        h->row_max, h->row_denom, s);
+  }
+  h->last_launches = take_launch_count();
+  return st;
+}
+
+llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q,
+                                 const void* k, const void* v, const float* out, float* dq,
+                                 float* dk, float* dv, void* stream) {
+  NONNULL(h);
+  NONNULL(d_out);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(out);
+  NONNULL(dq);
+  NONNULL(dk);
+  NONNULL(dv);
+  const Geometry& g = h->g;
+  cudaStream_t s = S(stream);
+  take_launch_count();
+  llsa_status st = transpose_all_impl(g, h->units, h->tables, h->csc_off, h->csc_flat,
+                                      h->tr_ws, s);
+  if (!st) {
+    if (h->tc)
+      st = tc_backward(g, h->units, d_out, out, h->row_max, h->row_denom, q, k, v, h->pyr_k,
+                       h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv, h->tcb,
+                       h->bwd_ws, s);
+    else
+      st = simt_backward(g, h->units, h->dt, d_out, out, h->row_max, h->row_denom, q, k, v,
+                         h->pyr_k, h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv,
+                         h->bwd_ws, s);
+  }
+  h->last_launches = take_launch_count();
+  return st;
+}
+
+llsa_status llsa_handle_buffer(llsa_handle h, llsa_buffer which, void** ptr, size_t* bytes) {
+  NONNULL(h);
+  NONNULL(ptr);
+  void* p[8] = {h->pyr_q, h->pyr_k, h->pyr_v, h->tables, h->csc_off, h->csc_flat, h->row_max,
+                h->row_denom};
+  if ((int)which < 0 || (int)which > 7) return fail(LLSA_ERR_ARGUMENT, "bad buffer id");
+  *ptr = p[which];
+  if (bytes) *bytes = h->sizes[which];
+  return LLSA_OK;
+}
+
+uint32_t llsa_handle_last_launches(llsa_handle h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"

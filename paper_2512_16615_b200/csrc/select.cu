@@ -1,0 +1,204 @@
+// K2/K3 — coarse-to-fine Top-K block selection, P/src/selection.cpp:21-179.
+//
+// Scores use the reference's exact fp32 recipe (dot4_exact: 4-lane
+// association, no FMA; then scale*dot), so selections are bit-identical to
+// the f32 reference.  Top-K is a rank selection: candidate c is kept iff
+//   #{c' : s[c'] > s[c]  or  (s[c'] == s[c] and c' < c)} < K,
+// which is exactly the (score desc, position asc) order of topk_row
+// (selection.cpp:21-38) with its lowest-index tie-break, computed without a
+// sort and with float comparisons (−0.0 ties +0.0).  Kept candidates are
+// emitted in ascending position order; candidate ids ascend with position
+// (parent rows are sorted), so rows come out ascending as the reference's
+// final std::sort makes them.
+//
+// select_level: one CTA per (unit, level-l query block).  All B query rows
+// of the block share the same K·B candidate tokens, so the CTA stages those
+// rows in shared memory once (row stride d+4 floats: conflict-free float4
+// reads) and scores B×K·B pairs from smem.
+#include "common.cuh"
+#include "internal.h"
+
+namespace llsa_impl {
+namespace {
+
+using namespace llsa_dev;
+
+__device__ __forceinline__ bool beats(float sa, uint32_t a, float sb, uint32_t b) {
+  // true when candidate a ranks before candidate b
+  return sa > sb || (sa == sb && a < b);
+}
+
+// Rank-select over scores[0..C) held in smem; writes selected flags.
+__device__ void rank_select(const float* scores, uint32_t C, uint32_t K, uint8_t* sel,
+                            uint32_t tid, uint32_t nthr) {
+  for (uint32_t c = tid; c < C; c += nthr) {
+    const float s = scores[c];
+    uint32_t rank = 0;
+    for (uint32_t c2 = 0; c2 < C; ++c2) rank += beats(scores[c2], c2, s, c) ? 1u : 0u;
+    sel[c] = rank < K ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) select_coarsest_kernel(
+    const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
+    uint64_t k_unit_stride, uint32_t rows, uint32_t C, uint32_t d, uint32_t K,
+    float scale, uint32_t* __restrict__ out, uint64_t out_unit_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t row = blockIdx.x;
+  const uint32_t unit = blockIdx.y;
+  float* sq = reinterpret_cast<float*>(smem);                 // d (padded to 4)
+  float* scores = sq + ((d + 3) & ~3u);                        // C
+  uint8_t* sel = reinterpret_cast<uint8_t*>(scores + C);       // C
+  const float* qr = q + unit * q_unit_stride + (uint64_t)row * d;
+  const float* ku = k + unit * k_unit_stride;
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) sq[j] = qr[j];
+  __syncthreads();
+  const bool v4 = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(ku) % 16 == 0);
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const float* kr = ku + (uint64_t)c * d;
+    const float dot = v4 ? dot4_exact_v4(reinterpret_cast<const float4*>(sq),
+                                         reinterpret_cast<const float4*>(kr), d / 4)
+                         : dot4_exact(sq, kr, d);
+    scores[c] = __fmul_rn(scale, dot);
+  }
+  __syncthreads();
+  rank_select(scores, C, K, sel, threadIdx.x, blockDim.x);
+  __syncthreads();
+  uint32_t* o = out + unit * out_unit_stride + (uint64_t)row * K;
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    if (!sel[c]) continue;
+    uint32_t pos = 0;
+    for (uint32_t c2 = 0; c2 < c; ++c2) pos += sel[c2];
+    o[pos] = c;
+  }
+}
+
+__global__ void __launch_bounds__(256) select_level_kernel(
+    const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
+    uint64_t k_unit_stride, const uint32_t* __restrict__ parent,
+    uint64_t parent_unit_stride, uint32_t parent_k, uint32_t key_blocks, uint32_t d,
+    uint32_t K, float scale, uint32_t B, bool stage_k, uint32_t* __restrict__ out,
+    uint64_t out_unit_stride, uint32_t* flag) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t blk = blockIdx.x;   // level-l query block (= parent row)
+  const uint32_t unit = blockIdx.y;
+  const uint32_t C = parent_k * B;
+  const uint32_t ld = (d + 3) & ~3u;           // q row stride
+  const uint32_t ldk = ((d + 3) & ~3u) + 4;    // padded k row stride
+  uint32_t* ids = reinterpret_cast<uint32_t*>(smem);            // C
+  float* sq = reinterpret_cast<float*>(ids + ((C + 3) & ~3u));  // B * ld
+  float* scores = sq + (uint64_t)B * ld;                        // B * C
+  uint8_t* sel = reinterpret_cast<uint8_t*>(scores + (((uint64_t)B * C + 3) & ~3ull));  // B * C
+  float* sk = reinterpret_cast<float*>(sel + (((uint64_t)B * C + 15) & ~15ull));  // C * ldk
+
+  const uint32_t* prow = parent + unit * parent_unit_stride + (uint64_t)blk * parent_k;
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    uint32_t pb = prow[c / B];
+    if (pb >= key_blocks) {  // IndexOutOfRange, selection.cpp:125-130
+      raise_flag(flag, kErrIndex);
+      pb = 0;
+    }
+    ids[c] = pb * B + c % B;
+  }
+  const float* qu = q + unit * q_unit_stride + (uint64_t)blk * B * d;
+  for (uint32_t e = threadIdx.x; e < B * d; e += blockDim.x)
+    sq[(e / d) * ld + e % d] = qu[e];
+  __syncthreads();
+  const float* ku = k + unit * k_unit_stride;
+  if (stage_k) {
+    for (uint64_t e = threadIdx.x; e < (uint64_t)C * d; e += blockDim.x) {
+      const uint32_t c = (uint32_t)(e / d), j = (uint32_t)(e % d);
+      sk[(uint64_t)c * ldk + j] = ku[(uint64_t)ids[c] * d + j];
+    }
+  }
+  __syncthreads();
+  const bool v4 = stage_k && (d % 4 == 0);
+  for (uint32_t p = threadIdx.x; p < B * C; p += blockDim.x) {
+    const uint32_t r = p / C, c = p % C;
+    float dot;
+    if (v4) {
+      dot = dot4_exact_v4(reinterpret_cast<const float4*>(sq + r * ld),
+                          reinterpret_cast<const float4*>(sk + (uint64_t)c * ldk), d / 4);
+    } else {
+      const float* kr = stage_k ? sk + (uint64_t)c * ldk : ku + (uint64_t)ids[c] * d;
+      dot = dot4_exact(sq + r * ld, kr, d);
+    }
+    scores[p] = __fmul_rn(scale, dot);
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < B * C; p += blockDim.x) {
+    const uint32_t r = p / C, c = p % C;
+    const float* sr = scores + (uint64_t)r * C;
+    const float s = sr[c];
+    uint32_t rank = 0;
+    for (uint32_t c2 = 0; c2 < C; ++c2) rank += beats(sr[c2], c2, s, c) ? 1u : 0u;
+    sel[p] = rank < K ? 1 : 0;
+  }
+  __syncthreads();
+  uint32_t* o = out + unit * out_unit_stride + (uint64_t)blk * B * K;
+  for (uint32_t p = threadIdx.x; p < B * C; p += blockDim.x) {
+    if (!sel[p]) continue;
+    const uint32_t r = p / C, c = p % C;
+    const uint8_t* sr = sel + (uint64_t)r * C;
+    uint32_t pos = 0;
+    for (uint32_t c2 = 0; c2 < c; ++c2) pos += sr[c2];
+    o[(uint64_t)r * K + pos] = ids[c];
+  }
+}
+
+}  // namespace
+
+llsa_status launch_select_coarsest(const float* q, uint64_t q_unit_stride, const float* k,
+                                   uint64_t k_unit_stride, uint32_t units, uint32_t rows,
+                                   uint32_t cands, uint32_t d, uint32_t K, float scale,
+                                   uint32_t* out, uint64_t out_unit_stride, cudaStream_t s) {
+  if (rows == 0 || units == 0) return LLSA_OK;
+  const size_t smem = sizeof(float) * (((d + 3) & ~3u) + cands) + cands + 16;
+  if (smem > 200 * 1024)
+    return fail(LLSA_ERR_UNSUPPORTED, "select_coarsest: %u candidates exceed shared memory",
+                cands);
+  if (smem > 48 * 1024)
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(select_coarsest_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+  select_coarsest_kernel<<<dim3(rows, units), 256, smem, s>>>(
+      q, q_unit_stride, k, k_unit_stride, rows, cands, d, K, scale, out, out_unit_stride);
+  count_launch();
+  LLSA_LAUNCH_CHECK("select_coarsest_kernel");
+  return LLSA_OK;
+}
+
+llsa_status launch_select_level(const float* q, uint64_t q_unit_stride, const float* k,
+                                uint64_t k_unit_stride, const uint32_t* parent,
+                                uint64_t parent_unit_stride, uint32_t units,
+                                uint32_t parent_rows, uint32_t parent_k, uint64_t k_rows,
+                                uint32_t d, uint32_t K, float scale, uint32_t B,
+                                uint32_t* out, uint64_t out_unit_stride, cudaStream_t s) {
+  if (parent_rows == 0 || units == 0) return LLSA_OK;
+  const uint64_t C = (uint64_t)parent_k * B;
+  const uint64_t ld = (d + 3) & ~3u, ldk = ld + 4;
+  const uint64_t base = 4 * ((C + 3) & ~3ull) + 4 * B * ld + 4 * ((B * C + 3) & ~3ull) +
+                        ((B * C + 15) & ~15ull);
+  uint64_t smem = base + 4 * C * ldk;
+  bool stage = true;
+  if (smem > 200 * 1024) {
+    stage = false;
+    smem = base;
+  }
+  if (smem > 200 * 1024)
+    return fail(LLSA_ERR_UNSUPPORTED, "select_level: block of %u rows x %llu candidates "
+                "exceeds shared memory", B, (unsigned long long)C);
+  if (smem > 48 * 1024)
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(select_level_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+  const uint32_t key_blocks = (uint32_t)(k_rows / B);
+  select_level_kernel<<<dim3(parent_rows, units), 256, smem, s>>>(
+      q, q_unit_stride, k, k_unit_stride, parent, parent_unit_stride, parent_k, key_blocks,
+      d, K, scale, B, stage, out, out_unit_stride, device_flag());
+  count_launch();
+  LLSA_LAUNCH_CHECK("select_level_kernel");
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl

@@ -1,0 +1,37 @@
+// Tensor-core attention path (d = 64, B = 16, bf16 inputs): interface used
+// by the handle API in capi.cu.  Implementation: attn_tc.cu.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace llsa_impl {
+
+// Per-handle scratch of the tensor-core path.
+struct TcBuffers {
+  // Coarse levels 1..L, pre-scaled by the level's key/value gain and split
+  // into bf16 hi + lo parts (SURVEY.md hard part 3): [units][pyr_rows][64].
+  __nv_bfloat16* k_hi = nullptr;
+  __nv_bfloat16* k_lo = nullptr;
+  __nv_bfloat16* v_hi = nullptr;
+  __nv_bfloat16* v_lo = nullptr;
+};
+
+bool tc_supported(const Geometry& g, llsa_dtype dt);
+size_t tc_buffer_bytes(const Geometry& g, uint32_t units);
+void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out);
+
+llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
+                       const void* v, const float* pyr_k, const float* pyr_v,
+                       const uint32_t* tables, float* out, float* row_max, float* row_denom,
+                       const TcBuffers& tb, cudaStream_t s);
+size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units);
+llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
+                        const float* out, const float* row_max, const float* row_denom,
+                        const void* q, const void* k, const void* v, const float* pyr_k,
+                        const float* pyr_v, const uint32_t* tables,
+                        const uint32_t* csc_offsets, const uint32_t* csc_flat, float* dq,
+                        float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s);
+
+}  // namespace llsa_impl

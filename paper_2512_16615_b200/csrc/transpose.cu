@@ -1,0 +1,169 @@
+// K4 — CSR → CSC index transposition (Alg. 2), P/src/indexmap.cpp:14-88.
+//
+// Same three linear passes as the reference — count, exclusive prefix sum,
+// scatter — then each segment is put into the canonical ascending order.
+// Instead of the reference's per-segment std::sort, each element's final slot
+// is its rank inside the segment (#elements smaller, ties by scatter slot),
+// computed by one warp per key block: no second sort pass, deterministic for
+// any scatter order.  Integer-only, HBM/latency-bound and tiny (T·K entries).
+#include "common.cuh"
+#include "internal.h"
+
+namespace llsa_impl {
+namespace {
+
+using namespace llsa_dev;
+
+__global__ void count_kernel(const uint32_t* __restrict__ idx, uint64_t idx_unit_stride,
+                             uint64_t per_unit, uint32_t units, uint32_t key_blocks,
+                             uint32_t* __restrict__ counts, uint32_t* flag) {
+  const uint64_t total = per_unit * units;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e / per_unit, i = e - u * per_unit;
+    const uint32_t b = idx[u * idx_unit_stride + i];
+    if (b >= key_blocks) {  // indexmap.cpp:28-38
+      raise_flag(flag, kErrIndex);
+      continue;
+    }
+    atomicAdd(&counts[u * key_blocks + b], 1u);
+  }
+}
+
+// One CTA per unit: exclusive scan of counts → offsets[0..key_blocks], and
+// the scatter cursors (= offsets) written back over counts.
+__global__ void __launch_bounds__(1024) scan_kernel(uint32_t* __restrict__ counts,
+                                                    uint32_t key_blocks,
+                                                    uint32_t* __restrict__ offsets,
+                                                    uint64_t off_unit_stride) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  const uint32_t u = blockIdx.x;
+  uint32_t* cnt = counts + (uint64_t)u * key_blocks;
+  uint32_t* off = offsets + (uint64_t)u * off_unit_stride;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < key_blocks; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < key_blocks ? cnt[i] : 0u;
+    uint32_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= (uint32_t)o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - v;
+    if (i < key_blocks) {
+      off[i] = excl;
+      cnt[i] = excl;  // cursor
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[key_blocks] = carry;
+}
+
+__global__ void scatter_kernel(const uint32_t* __restrict__ idx, uint64_t idx_unit_stride,
+                               uint32_t rows, uint32_t k, uint32_t units,
+                               uint32_t key_blocks, uint32_t* __restrict__ cursor,
+                               uint32_t* __restrict__ tmp, uint64_t tmp_unit_stride) {
+  const uint64_t per_unit = (uint64_t)rows * k;
+  const uint64_t total = per_unit * units;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e / per_unit, i = e - u * per_unit;
+    const uint32_t b = idx[u * idx_unit_stride + i];
+    if (b >= key_blocks) continue;
+    const uint32_t pos = atomicAdd(&cursor[u * key_blocks + b], 1u);
+    tmp[u * tmp_unit_stride + pos] = (uint32_t)(i / k);
+  }
+}
+
+// One warp per (unit, key block): out[off + rank(e)] = tmp[e].
+__global__ void segment_order_kernel(const uint32_t* __restrict__ tmp,
+                                     uint64_t tmp_unit_stride,
+                                     const uint32_t* __restrict__ offsets,
+                                     uint64_t off_unit_stride, uint32_t key_blocks,
+                                     uint32_t units, uint32_t* __restrict__ flat,
+                                     uint64_t flat_unit_stride) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp >= (uint64_t)key_blocks * units) return;
+  const uint64_t u = warp / key_blocks, b = warp - u * key_blocks;
+  const uint32_t* off = offsets + u * off_unit_stride;
+  const uint32_t s0 = off[b], s1 = off[b + 1];
+  const uint32_t* seg = tmp + u * tmp_unit_stride + s0;
+  uint32_t* dst = flat + u * flat_unit_stride + s0;
+  const uint32_t len = s1 - s0;
+  for (uint32_t e = lane; e < len; e += 32) {
+    const uint32_t v = seg[e];
+    uint32_t rank = 0;
+    for (uint32_t e2 = 0; e2 < len; ++e2) {
+      const uint32_t w = seg[e2];
+      rank += (w < v || (w == v && e2 < e)) ? 1u : 0u;
+    }
+    dst[rank] = v;
+  }
+}
+
+unsigned grid_for(uint64_t threads, int block) {
+  uint64_t blocks = (threads + block - 1) / block;
+  const uint64_t cap = 148ull * 16;
+  return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
+}
+
+}  // namespace
+
+size_t transpose_ws_bytes(uint32_t units, uint32_t rows, uint32_t k, uint32_t key_blocks) {
+  const size_t a = ((size_t)units * key_blocks * 4 + 255) & ~size_t(255);
+  const size_t b = ((size_t)units * rows * k * 4 + 255) & ~size_t(255);
+  return a + b + 256;
+}
+
+llsa_status launch_transpose(const uint32_t* idx, uint64_t idx_unit_stride, uint32_t units,
+                             uint32_t rows, uint32_t k, uint32_t key_blocks,
+                             uint32_t* offsets, uint64_t off_unit_stride, uint32_t* flat,
+                             uint64_t flat_unit_stride, void* ws, cudaStream_t s) {
+  if (units == 0) return LLSA_OK;
+  uint32_t* counts = static_cast<uint32_t*>(ws);
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(
+      static_cast<char*>(ws) + (((size_t)units * key_blocks * 4 + 255) & ~size_t(255)));
+  const uint64_t per_unit = (uint64_t)rows * k;
+  if (key_blocks) LLSA_CUDA_TRY(cudaMemsetAsync(counts, 0, (size_t)units * key_blocks * 4, s));
+  if (per_unit && key_blocks) {
+    count_kernel<<<grid_for(per_unit * units, 256), 256, 0, s>>>(
+        idx, idx_unit_stride, per_unit, units, key_blocks, counts, device_flag());
+    count_launch();
+    LLSA_LAUNCH_CHECK("count_kernel");
+  }
+  scan_kernel<<<units, 1024, 0, s>>>(counts, key_blocks, offsets, off_unit_stride);
+  count_launch();
+  LLSA_LAUNCH_CHECK("scan_kernel");
+  if (per_unit == 0 || key_blocks == 0) return LLSA_OK;
+  scatter_kernel<<<grid_for(per_unit * units, 256), 256, 0, s>>>(
+      idx, idx_unit_stride, rows, k, units, key_blocks, counts, tmp, per_unit);
+  count_launch();
+  LLSA_LAUNCH_CHECK("scatter_kernel");
+  const uint64_t warps = (uint64_t)key_blocks * units;
+  segment_order_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+      tmp, per_unit, offsets, off_unit_stride, key_blocks, units, flat, flat_unit_stride);
+  count_launch();
+  LLSA_LAUNCH_CHECK("segment_order_kernel");
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl

@@ -1,0 +1,295 @@
+"""GPU parity: every CUDA stage against the oracle (the C restatement pinned
+to the reference in test_oracle.py) and the reference's golden fixtures.
+
+Bars: pyramids, selection tables, CSC lists and plans are
+bit-exact; attention outputs and gradients within rel 1e-3 (fp32 inputs) or
+2e-2 (bf16 inputs), measured as max|Δ|/max|ref| against the fp32 oracle run
+on the same (bf16-widened) inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_16615_b200 as llsa
+from oracle import Config, bf16_round, lse, rel_err, unit_inputs
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+DEV = "cuda"
+
+
+def T(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+
+
+def U32(t):
+    return t.cpu().numpy().astype(np.uint32)
+
+
+def vcfg(c: Config):
+    return llsa.validate_config(llsa.LLSAConfig(c.n, c.d, c.block_size, c.top_k, c.levels,
+                                                c.enrich_levels, c.softmax_scale,
+                                                c.reweight_mode, c.safe_softmax))
+
+
+# ---------------------------------------------------------------- compression
+@pytest.mark.parametrize("rows,d,b,L,bf", [(64, 5, 4, 2, False), (81, 3, 3, 3, False),
+                                           (4096, 64, 16, 2, True), (65536, 64, 16, 3, True),
+                                           (1024, 32, 4, 4, False), (256, 6, 2, 7, True)])
+def test_pyramid_bit_exact(oracle_c, rows, d, b, L, bf):
+    x = oracle_c.gen_random(rows, d, 31337 + rows)
+    if bf:
+        x = bf16_round(x)
+    got = llsa.build_pyramid(T(x, torch.bfloat16 if bf else torch.float32), b, L)
+    want = oracle_c.build_pyramid(x, b, L)
+    np.testing.assert_array_equal(got[0].cpu().numpy(), want)
+
+
+def test_pyramid_kats(golden):
+    for case in golden["kats"]["pyramid"]:
+        x = T(np.array(case["x"], np.float32)[:, None])
+        flat = llsa.build_pyramid(x, case["B"], case["L"])
+        lv = llsa.pyramid_levels(flat, len(case["x"]), case["B"], case["L"])
+        assert lv[case["level"] - 1][0, :, 0].cpu().tolist() == case["expect"]
+    with pytest.raises(llsa.DivisibilityError):
+        llsa.build_pyramid(T(np.ones((6, 1), np.float32)), 2, 2)
+
+
+def test_pool_backward(oracle_c, golden):
+    for case in golden["kats"]["pool_backward"]:
+        out = llsa.pool_backward(T(np.array(case["g"], np.float32)[:, None]), case["B"],
+                                 case["hops"])
+        assert out[0, :, 0].cpu().tolist() == case["expect"]
+    g = oracle_c.gen_random(16, 8, 5)
+    for hops in (0, 1, 2):
+        np.testing.assert_array_equal(llsa.pool_backward(T(g), 4, hops)[0].cpu().numpy(),
+                                      oracle_c.pool_backward(g, 4, hops))
+
+
+# ---------------------------------------------------------------- selection
+def test_select_coarsest_bit_exact(oracle_c):
+    for rows, cands, d, k, scale in ((12, 20, 6, 5, 0.33), (16, 16, 64, 8, 0.125),
+                                     (256, 256, 64, 8, 0.125), (6, 8, 4, 8, 1.0),
+                                     (64, 64, 64, 16, 0.125)):
+        q = oracle_c.gen_random(rows, d, 21)
+        kk = oracle_c.gen_random(cands, d, 22)
+        got = llsa.select_coarsest(T(q), T(kk), k, scale)
+        np.testing.assert_array_equal(U32(got[0]), oracle_c.select_coarsest(q, kk, k, scale))
+
+
+def test_ties_break_to_smaller_index(golden, oracle_c):
+    t = golden["kats"]["ties"]
+    kk = np.tile(np.array(t["key_row"], np.float32), (t["key_rows"], 1))
+    q = oracle_c.gen_random(t["q_rows"], t["d"], t["q_seed"])
+    got = U32(llsa.select_coarsest(T(q), T(kk), t["top_k"], 1.0)[0])
+    assert (got == np.array(t["expect_row"])).all()
+    # exact-zero scores (all-zero pooled rows, e.g. padding) tie too
+    z = np.zeros((32, 8), np.float32)
+    got = U32(llsa.select_coarsest(T(z[:4]), T(z), 4, 0.125)[0])
+    assert (got == np.arange(4)).all()
+
+
+def test_select_level_bit_exact_and_validation(oracle_c):
+    q = oracle_c.gen_random(16, 4, 5)
+    kk = oracle_c.gen_random(16, 4, 6)
+    parent = np.array([[0, 2], [1, 3], [0, 1], [2, 3]], np.uint32)
+    got = llsa.select_level(T(q), T(kk), T(parent, torch.int32), 1, 3, 0.7, 4)
+    np.testing.assert_array_equal(U32(got[0]), oracle_c.select_level(q, kk, parent, 1, 3, 0.7, 4))
+    with pytest.raises(llsa.LevelError):
+        llsa.select_level(T(q), T(kk), T(parent, torch.int32), 0, 2, 1.0, 4)
+    with pytest.raises(llsa.ShapeMismatch):
+        llsa.select_level(T(q[:12]), T(kk), T(parent, torch.int32), 1, 2, 1.0, 4)
+    with pytest.raises(llsa.TopKError):
+        llsa.select_level(T(q), T(kk), T(parent, torch.int32), 1, 9, 1.0, 4)
+    bad = parent.copy()
+    bad[1, 1] = 4
+    llsa.select_level(T(q), T(kk), T(bad, torch.int32), 1, 2, 1.0, 4)
+    with pytest.raises(llsa.IndexOutOfRange):
+        llsa.sync_status()
+
+
+@pytest.mark.parametrize("name", ["c1_n4096_L1", "c1_n4096_L2", "c2_n16384_L2",
+                                  "c3_n65536_L3", "c3p_n65536_L2"])
+def test_hierarchical_topk_matches_reference_tables(golden, oracle_c, name):
+    g = golden["tables"]
+    n, d, b, k, L, le, seed = (int(x) for x in g[f"{name}/cfg"])
+    cfg = vcfg(Config(n, d, b, k, L, le))
+    q, kk = (bf16_round(oracle_c.gen_random(n, d, seed + i)) for i in range(2))
+    pq = llsa.build_pyramid(T(q, torch.bfloat16), b, L)
+    pk = llsa.build_pyramid(T(kk, torch.bfloat16), b, L)
+    tables = llsa.hierarchical_topk(pq, pk, cfg)
+    np.testing.assert_array_equal(U32(tables[0]), g[f"{name}/tables"])
+
+
+def test_hierarchical_topk_batched_units(oracle_c):
+    cfg = Config(4096, 64, 16, 8, 2, 2)
+    qs, ks, want = [], [], []
+    for u in range(3):
+        q, kk, _, _ = unit_inputs(cfg, u, backend=oracle_c)
+        qs.append(q)
+        ks.append(kk)
+        want.append(oracle_c.run(cfg, q, kk, kk).tables)
+    vc = vcfg(cfg)
+    pq = llsa.build_pyramid(T(np.stack(qs), torch.bfloat16), 16, 2)
+    pk = llsa.build_pyramid(T(np.stack(ks), torch.bfloat16), 16, 2)
+    got = U32(llsa.hierarchical_topk(pq, pk, vc))
+    for u in range(3):
+        np.testing.assert_array_equal(got[u], want[u])
+
+
+# ---------------------------------------------------------------- transpose
+def test_transpose_kats(golden):
+    for case in golden["kats"]["transpose"]:
+        idx = np.array(case["idx"], np.int32).reshape(case["rows"], case["k"])
+        offs, flat = llsa.transpose_indices(T(idx, torch.int32), case["key_blocks"])
+        assert offs[0].cpu().tolist() == case["offsets"]
+        assert flat[0].cpu().tolist() == case["flat"]
+
+
+def test_transpose_random_tables_match_oracle(oracle_c):
+    # acceptance A4 (P/tests/acceptance.cpp:168-217): random tables, exact
+    rng = np.random.default_rng(2024)
+    for _ in range(60):
+        qb, kb = int(rng.integers(1, 65)), int(rng.integers(1, 65))
+        k = int(rng.integers(1, min(8, kb) + 1))
+        idx = np.stack([np.sort(rng.permutation(kb)[:k]) for _ in range(qb)]).astype(np.uint32)
+        o, f = llsa.transpose_indices(T(idx.astype(np.int32), torch.int32), kb)
+        wo, wf = oracle_c.transpose(idx, kb)
+        np.testing.assert_array_equal(U32(o[0]), wo)
+        np.testing.assert_array_equal(U32(f[0]), wf)
+
+
+def test_transpose_degenerate_long_segment(oracle_c):
+    # every row picks the same blocks (constant keys → tie-break): segments = T
+    idx = np.tile(np.arange(8, dtype=np.uint32), (4096, 1))
+    o, f = llsa.transpose_indices(T(idx.astype(np.int32), torch.int32), 4096)
+    wo, wf = oracle_c.transpose(idx, 4096)
+    np.testing.assert_array_equal(U32(o[0]), wo)
+    np.testing.assert_array_equal(U32(f[0]), wf)
+
+
+def test_transpose_out_of_range_flags():
+    idx = np.array([[0], [5]], np.int32)
+    llsa.transpose_indices(T(idx, torch.int32), 4)
+    with pytest.raises(llsa.IndexOutOfRange):
+        llsa.sync_status()
+
+
+# ---------------------------------------------------------------- forward / backward
+SMALL = [Config(256, 8, 4, 2, 2, 2), Config(256, 8, 4, 2, 2, 2, reweight_mode=1),
+         Config(128, 8, 4, 2, 2, 0), Config(128, 8, 4, 2, 2, 1),
+         Config(64, 8, 4, 16, 1, 0), Config(256, 8, 4, 2, 2, 2, safe_softmax=False),
+         Config(1024, 16, 4, 4, 3, 3), Config(512, 33, 8, 3, 1, 1),
+         Config(4096, 64, 16, 8, 1, 1), Config(4096, 64, 16, 8, 2, 2)]
+
+
+def _staged(oracle_c, cfg: Config, seed: int, bf: bool):
+    q, k, v, dO = (oracle_c.gen_random(cfg.n, cfg.d, seed + i) for i in range(4))
+    if bf:
+        q, k, v, dO = (bf16_round(a) for a in (q, k, v, dO))
+    ref = oracle_c.run(cfg, q, k, v, dO)
+    dt = torch.bfloat16 if bf else torch.float32
+    vc = vcfg(cfg)
+    tq, tk, tv, tdo = (T(a, dt) for a in (q, k, v, dO))
+    pk = llsa.build_pyramid(tk, cfg.block_size, cfg.levels)
+    pv = llsa.build_pyramid(tv, cfg.block_size, cfg.levels)
+    pq = llsa.build_pyramid(tq, cfg.block_size, cfg.levels)
+    tables = llsa.hierarchical_topk(pq, pk, vc)
+    return ref, vc, (tq, tk, tv, tdo), pk, pv, tables
+
+
+@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: f"n{c.n}d{c.d}B{c.block_size}L{c.levels}"
+                         f"e{c.enrich_levels}m{c.reweight_mode}s{int(c.safe_softmax)}")
+@pytest.mark.parametrize("bf", [False, True])
+def test_staged_path_matches_oracle(oracle_c, cfg, bf):
+    ref, vc, (tq, tk, tv, tdo), pk, pv, tables = _staged(oracle_c, cfg, 100 + cfg.n, bf)
+    np.testing.assert_array_equal(U32(tables[0]), ref.tables)
+    lv, bl, w = llsa.build_plan(tables, vc)
+    np.testing.assert_array_equal(U32(lv[0]).reshape(-1), ref.plan_level)
+    np.testing.assert_array_equal(U32(bl[0]).reshape(-1), ref.plan_block)
+    np.testing.assert_array_equal(w[0].cpu().numpy().reshape(-1), ref.plan_weight)
+    st = llsa.llsa_forward(tq, tk, tv, pk, pv, tables, vc)
+    tol = 1e-4   # fp32 math on identical inputs: rounding-level agreement
+    assert rel_err(st.output[0].cpu().numpy(), ref.out)["max_rel"] <= tol
+    np.testing.assert_allclose(lse(st.row_max[0].cpu().numpy(), st.row_denom[0].cpu().numpy()),
+                               lse(ref.row_max, ref.row_denom), rtol=1e-5, atol=1e-4)
+    tr = llsa.transpose_all(tables, vc)
+    np.testing.assert_array_equal(U32(tr[0][0]), ref.csc_offsets)
+    np.testing.assert_array_equal(U32(tr[1][0]), ref.csc_flat)
+    dq, dk, dv = llsa.llsa_backward(tdo, st, tq, tk, tv, pk, pv, tables, tr, vc)
+    for name, got, want in (("dq", dq, ref.dq), ("dk", dk, ref.dk), ("dv", dv, ref.dv)):
+        e = rel_err(got[0].cpu().numpy(), want)
+        assert e["max_rel"] <= 1e-3, (name, e)
+    dk2, dv2 = llsa.kv_backward(tdo, st, tq, tk, tv, pk, pv, tr, vc)
+    assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
+
+
+def test_forward_overflow_without_rescaling_raises():
+    # P/tests/test_attention.cpp:180-223
+    q = np.full((16, 8), 300.0, np.float32)
+    k = np.ones((16, 8), np.float32)
+    from oracle import OracleC
+    v = OracleC().gen_random(16, 8, 31)
+    for safe, raises in ((False, True), (True, False)):
+        vc = llsa.validate_config(llsa.LLSAConfig(16, 8, 4, 2, 1, 0, safe_softmax=safe))
+        pq, pk, pv = (llsa.build_pyramid(T(a), 4, 1) for a in (q, k, v))
+        tables = llsa.hierarchical_topk(pq, pk, vc)
+        if raises:
+            with pytest.raises(llsa.NonFiniteError):
+                llsa.llsa_forward(T(q), T(k), T(v), pk, pv, tables, vc)
+        else:
+            st = llsa.llsa_forward(T(q), T(k), T(v), pk, pv, tables, vc)
+            assert torch.isfinite(st.output).all()
+
+
+def test_zero_cotangent_gives_zero_gradients(oracle_c):
+    cfg = Config(64, 4, 4, 2, 2, 2)
+    ref, vc, (tq, tk, tv, tdo), pk, pv, tables = _staged(oracle_c, cfg, 3, False)
+    st = llsa.llsa_forward(tq, tk, tv, pk, pv, tables, vc)
+    tr = llsa.transpose_all(tables, vc)
+    grads = llsa.llsa_backward(torch.zeros_like(tdo), st, tq, tk, tv, pk, pv, tables, tr, vc)
+    for g in grads:
+        assert (g == 0).all()
+
+
+# ---------------------------------------------------------------- fused handle
+@pytest.mark.parametrize("cfg,bf", [(Config(4096, 64, 16, 8, 1, 1), False),
+                                    (Config(4096, 64, 16, 8, 2, 2), True),
+                                    (Config(16384, 64, 16, 8, 2, 2), True),
+                                    (Config(16384, 64, 16, 8, 2, 2, reweight_mode=1), True),
+                                    (Config(16384, 64, 16, 8, 2, 0), True),
+                                    (Config(65536, 64, 16, 8, 3, 3), True)])
+def test_handle_path_matches_oracle(oracle_c, cfg, bf):
+    units = 2
+    ins = [unit_inputs(cfg, u, bf16=bf, backend=oracle_c) for u in range(units)]
+    want_bwd = cfg.n <= 16384
+    refs = [oracle_c.run(cfg, q, k, v, dO if want_bwd else None) for q, k, v, dO in ins]
+    dt = torch.bfloat16 if bf else torch.float32
+    q, k, v, dO = (T(np.stack([i[j] for i in ins]), dt) for j in range(4))
+    h = llsa.LLSAHandle(llsa.LLSAConfig(cfg.n, cfg.d, cfg.block_size, cfg.top_k, cfg.levels,
+                                        cfg.enrich_levels,
+                                        reweight_mode=cfg.reweight_mode), units, dt)
+    out = h.forward(q, k, v)
+    tol = 2e-2 if bf else 1e-3
+    tables = U32(h.view("tables"))
+    for u in range(units):
+        np.testing.assert_array_equal(tables[u], refs[u].tables)
+        e = rel_err(out[u].cpu().numpy(), refs[u].out)
+        assert e["max_rel"] <= tol, ("out", u, e)
+    if want_bwd:
+        dq, dk, dv = h.backward(dO, q, k, v, out)
+        llsa.sync_status()
+        for u in range(units):
+            for name, got, want in (("dq", dq, refs[u].dq), ("dk", dk, refs[u].dk),
+                                    ("dv", dv, refs[u].dv)):
+                e = rel_err(got[u].cpu().numpy(), want)
+                assert e["max_rel"] <= tol, (name, u, e)
+        # determinism: a second run is bitwise identical
+        out2 = h.forward(q, k, v)
+        g2 = h.backward(dO, q, k, v, out2)
+        assert torch.equal(out, out2)
+        for a, b in zip((dq, dk, dv), g2):
+            assert torch.equal(a, b)
