@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""LLSA hot-path benchmark (BASELINE.json metric: "LLSA fwd+bwd ms at
+N=65536 (256² px tokens) and % of tensor/HBM roofline").
+
+One step = the whole path on `units` = 16 (batch·head) units per GPU:
+compress → select → attention forward → CSR→CSC transpose → backward, at
+N=65536, d=64, B=16, K=8, L=3 (= "4 levels"), L_e=L, ScaleKV, bf16 inputs,
+synthetic N(0,1) data resident in HBM.  Multi-GPU (torchrun): every rank runs
+its own 16 units (weak scaling over batch; no collective on the data path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl llsa|reference]
+
+Prints ONE JSON line on rank 0 (see the task contract; DESIGN.md §Measurement
+explains every field).  `--impl reference` times the reference CPU library
+(oracle/_ref, built from /root/reference) with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TOK, D, B, K, LEVELS = 65536, 64, 16, 8, 3
+UNITS_PER_GPU = 16
+METRIC = "LLSA fwd+bwd ms at N=65536 (256² px tokens) and % of tensor/HBM roofline"
+
+
+def _peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback"
+
+
+def _geometry(n: int, L: int, k: int = K, b: int = B, d: int = D):
+    E = k * L + n // b ** (L + 1)
+    pairs = n * E * b                  # (query, key) pairs per unit, P = N·E·B
+    fine_pairs = n * k * b             # level-0 part
+    return E, pairs, fine_pairs
+
+
+def algorithmic_work(n: int, L: int, units: int) -> dict:
+    """Per-stage algorithmic work for `units` units."""
+    E, P, Pf = _geometry(n, L)
+    d = D
+    pyr_rows = sum(n // B ** l for l in range(1, L + 1))
+    sel_macs = (n // B ** L) ** 2 * d + sum((n // B ** l) * K * B * d for l in range(1, L))
+    return {
+        # bytes: read q,k,v bf16, write fp32 pyramids of the three
+        "compress": {"bytes": units * (3 * n * d * 2 + 3 * pyr_rows * d * 4), "flops": 0},
+        "select": {"bytes": units * (2 * pyr_rows * d * 4), "flops": units * 2 * sel_macs},
+        # forward: QK^T + PV = 4·d·P; bytes: q,k,v bf16 in, O fp32 + (m, l) out
+        "fwd_attention": {"flops": units * 4 * d * P,
+                          "bytes": units * (3 * n * d * 2 + n * d * 4 + 2 * n * 4)},
+        "transpose": {"bytes": units * 3 * 4 * sum((n // B ** (l + 1)) * K for l in range(L)),
+                      "flops": 0},
+        # backward: 10·d·P (S, dP, dV, dQ, dK); bytes: q,k,v,dO bf16 + O fp32 + stats in,
+        # dq,dk,dv fp32 out
+        "backward": {"flops": units * 10 * d * P,
+                     "bytes": units * (4 * n * d * 2 + n * d * 4 + 2 * n * 4 + 3 * n * d * 4)},
+        "pairs": units * P, "fine_pairs": units * Pf, "E": E,
+    }
+
+
+def stage_work(name: str, W: dict) -> dict:
+    """Algorithmic work attributed to one timed stage of the handle."""
+    if name in W and isinstance(W[name], dict):
+        return W[name]
+    bw = W["backward"]
+    P, Pf = W["pairs"], W["fine_pairs"]
+    if name in ("bwd_dq", "bwd_dq_tc"):          # S, dP, dQ over all pairs
+        return {"flops": bw["flops"] * 6 // 10, "bytes": bw["bytes"] // 2}
+    if name.startswith("bwd_kv_fine"):           # dK, dV over fine pairs
+        return {"flops": bw["flops"] * 4 // 10 * Pf // P, "bytes": bw["bytes"] // 3}
+    if name.startswith("bwd_kv"):                # dK, dV over coarse pairs
+        return {"flops": bw["flops"] * 4 // 10 * (P - Pf) // P, "bytes": bw["bytes"] // 6}
+    return {"flops": 0, "bytes": 0}
+
+
+class ClockSampler:
+    """Samples SM clocks + throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            pass
+        self.period = period_s
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                c = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((c, r))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self._t.join(timeout=1)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1): "gpu_idle",
+            getattr(nv, "nvmlClocksEventReasonApplicationsClocksSetting", 0x2): "app_clocks",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSyncBoost", 0x10): "sync_boost",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80):
+                "hw_power_brake_slowdown",
+        }
+        seen = 0
+        for _, r in self.samples:
+            seen |= r
+        reasons = sorted(v for k, v in names.items() if seen & k)
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+# ---------------------------------------------------------------------------
+def reference_sample(steps: int, warmup: int, n: int = N_TOK, L: int = LEVELS,
+                     units: int = UNITS_PER_GPU) -> dict:
+    """Times the reference library (oracle/_ref, all host threads) on one unit
+    of the workload per step; reports ms for the full `units`-unit step."""
+    import numpy as np
+
+    from oracle import REF_SO, Config, OracleC, Reference, unit_inputs
+    cfg = Config(n, D, B, K, L, L)
+    if os.path.exists(REF_SO[32]):
+        be = Reference(32)
+        be.set_threads(0)
+        kind, cores = "reference", be.threads()
+    else:  # reference not compiled on this box: the C restatement (1 thread)
+        be = OracleC()
+        kind, cores = "port", 1
+    q, k, v, dO = unit_inputs(cfg, 0, backend=be)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        be.run(cfg, q, k, v, dO, **({"want_outputs": False} if kind == "reference" else {}))
+        dt = (time.perf_counter() - t0) * 1e3
+        if i >= warmup:
+            times.append(dt)
+    per_unit = statistics.median(times)
+    return {"value": per_unit * units, "unit": "ms", "cores": cores, "kind": kind,
+            "sample": f"1 of {units} units per step (N={n}, L={L}, fwd+bwd incl. "
+                      f"compress/select/plan/transpose), median of {steps} after {warmup} "
+                      f"warm-up, x{units} units; {os.cpu_count()} host CPUs",
+            "per_unit_ms": per_unit}
+
+
+# ---------------------------------------------------------------------------
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="llsa", choices=["llsa", "reference"])
+    ap.add_argument("--n", type=int, default=N_TOK)
+    ap.add_argument("--levels", type=int, default=LEVELS)
+    ap.add_argument("--units", type=int, default=UNITS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_json = {"workload": f"LLSA fwd+bwd, N={args.n}, {args.units} units (batch·head) per "
+                            f"GPU, d=64, B=16, K=8, L={args.levels} (BASELINE '4 levels'), "
+                            "L_e=L, ScaleKV, bf16 in / fp32 out",
+                "n": args.n, "d": D, "block_size": B, "top_k": K, "levels": args.levels,
+                "enrich_levels": args.levels, "units_per_gpu": args.units,
+                "global_units": args.units * world, "parallelism": f"units/{world}gpu",
+                "l2": "inputs larger than L2 (4 x units x N x 64 bf16 per step)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = reference_sample(args.steps, args.warmup, args.n, args.levels, args.units)
+        line = {"metric": METRIC, "value": r["value"], "unit": "ms", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["value"], "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_random "
+                "N(0,1), bf16-rounded)", "config": cfg_json,
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "ms", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_16615_b200 as llsa
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    units = args.units
+    n = args.n
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    shape = (units, n, D)
+    q, k, v, dO = (torch.randn(shape, generator=gen, device=dev).to(torch.bfloat16)
+                   for _ in range(4))
+    cfg = llsa.LLSAConfig(n, D, B, K, args.levels, args.levels)
+    h = llsa.LLSAHandle(cfg, units, torch.bfloat16)
+    h.enable_timing(True)
+    out = torch.empty(shape, device=dev, dtype=torch.float32)
+    dq, dk, dv = (torch.empty(shape, device=dev, dtype=torch.float32) for _ in range(3))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        h.forward(q, k, v, out)
+        lf = h.last_launches
+        h.backward(dO, q, k, v, out, dq, dk, dv)
+        return lf + h.last_launches
+
+    for _ in range(args.warmup):
+        launches = step()
+    llsa.sync_status()
+    h.enable_timing(True)  # reset the event ring: stage times cover the timed region only
+
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            launches = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    stages = h.stage_times()
+    llsa.sync_status()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- roofline of the dominant kernel (stage) ----------------------------
+    peaks, peak_src = _peaks()
+    W = algorithmic_work(n, args.levels, units)
+    dom_name, dom_ms = max(stages, key=lambda s: s[1]) if stages else ("?", 0.0)
+    wk = stage_work(dom_name, W)
+    t_tc = wk["flops"] / (peaks["bf16_tflops"] * 1e12) if wk["flops"] else 0.0
+    t_hbm = wk["bytes"] / (peaks["hbm_gbs"] * 1e9) if wk["bytes"] else 0.0
+    if t_tc >= t_hbm:
+        achieved = wk["flops"] / (dom_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s"}
+    else:
+        achieved = wk["bytes"] / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom_name
+    roof["kernel_ms"] = dom_ms
+    roof["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json, burst)"
+    total_flops = W["fwd_attention"]["flops"] + W["backward"]["flops"]
+    ideal_ms = (max(W["fwd_attention"]["flops"] / (peaks["bf16_tflops"] * 1e12),
+                    W["fwd_attention"]["bytes"] / (peaks["hbm_gbs"] * 1e9)) +
+                max(W["backward"]["flops"] / (peaks["bf16_tflops"] * 1e12),
+                    W["backward"]["bytes"] / (peaks["hbm_gbs"] * 1e9))) * 1e3
+
+    # ---- end to end through the C ABI with host buffers -----------------------
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, dO))
+        ho, hdq, hdk, hdv = (torch.empty(shape, dtype=torch.float32).pin_memory()
+                             for _ in range(4))
+        dq_, dk_, dv_, dO_ = q.clone(), k.clone(), v.clone(), dO.clone()
+
+        def e2e_step():
+            for d_, h_ in ((dq_, hq), (dk_, hk), (dv_, hv), (dO_, hdo)):
+                d_.copy_(h_, non_blocking=True)
+            h.forward(dq_, dk_, dv_, out)
+            h.backward(dO_, dq_, dk_, dv_, out, dq, dk, dv)
+            for h_, d_ in ((ho, out), (hdq, dq), (hdk, dk), (hdv, dv)):
+                h_.copy_(d_, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        e2e_steps = max(3, min(args.steps, 10))
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4 * q.numel() * 2,
+               "d2h_bytes_per_step": 4 * out.numel() * 4, "steps": e2e_steps,
+               "path": "llsa_handle_forward/backward (C ABI) with pinned host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = reference_sample(1, 1, n, args.levels, units)
+            cpu = {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic (torch.randn N(0,1) -> bf16, resident in "
+                "HBM)", "config": cfg_json,
+                "units_per_s": units * world / (ms * 1e-3),
+                "effective_tflops": total_flops / (ms * 1e-3) / 1e12,
+                "ideal_ms": ideal_ms,
+                "roofline": roof,
+                "stages_ms": {s: round(t_, 4) for s, t_ in stages},
+                "tensor_cores": h.uses_tensor_cores,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

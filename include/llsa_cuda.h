@@ -228,6 +228,14 @@ llsa_status llsa_handle_buffer(llsa_handle h, llsa_buffer which, void** ptr,
                                size_t* bytes);
 /* Number of kernel launches the last forward / backward issued. */
 uint32_t llsa_handle_last_launches(llsa_handle h);
+/* Stage timing: when enabled, forward/backward record a CUDA event on the
+ * call's stream between stages (no synchronisation).  llsa_handle_stage_times
+ * synchronises on those events and returns up to `cap` (name, ms) pairs of
+ * the most recent forward followed by the most recent backward; names are
+ * static strings.  Returns the number of stages. */
+llsa_status llsa_handle_enable_timing(llsa_handle h, int enable);
+uint32_t llsa_handle_stage_times(llsa_handle h, const char** names, float* ms,
+                                 uint32_t cap);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,8 @@ SIGNATURES = {
     "llsa_handle_backward": (C.c_int, [_vp] + [_vp] * 8 + [_vp]),
     "llsa_handle_buffer": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_sz)]),
     "llsa_handle_last_launches": (_u32, [_vp]),
+    "llsa_handle_enable_timing": (C.c_int, [_vp, C.c_int]),
+    "llsa_handle_stage_times": (_u32, [_vp, C.POINTER(C.c_char_p), C.POINTER(C.c_float), _u32]),
 }
 
 

@@ -486,7 +486,8 @@ static llsa_status bwd_impl(const Geometry& g, uint32_t units, const void* d_out
                             const void* q_, const void* k, const void* v,
                             const float* pyr_k, const float* pyr_v, const uint32_t* tables,
                             const uint32_t* csc_offsets, const uint32_t* csc_flat,
-                            float* dq, float* dk, float* dv, void* ws, cudaStream_t s) {
+                            float* dq, float* dk, float* dv, void* ws, cudaStream_t s,
+                            StageMarker* mk) {
   const T* q = static_cast<const T*>(q_);
   const T* dout = static_cast<const T*>(d_out_);
   char* base = static_cast<char*>(ws);
@@ -499,11 +500,13 @@ static llsa_status bwd_impl(const Geometry& g, uint32_t units, const void* d_out
                                                                drow);
   count_launch();
   LLSA_LAUNCH_CHECK("drow_kernel");
+  LLSA_MARK(mk, "bwd_drow", s);
   if (dq) {
     dq_kernel<T, COLS><<<warps_grid(g.n * units), 256, 0, s>>>(
         D, units, q, dout, Kp, Vp, tables, row_max, row_denom, drow, dq);
     count_launch();
     LLSA_LAUNCH_CHECK("dq_kernel");
+    LLSA_MARK(mk, "bwd_dq", s);
   }
   // level 0: straight into dk/dv (attention_grad.cpp:127-135)
   kv_kernel<T, COLS><<<warps_grid(g.n * units), 256, 0, s>>>(
@@ -512,6 +515,7 @@ static llsa_status bwd_impl(const Geometry& g, uint32_t units, const void* d_out
       Kp, Vp, row_max, row_denom, drow, dk, dv, g.n * g.d, 0);
   count_launch();
   LLSA_LAUNCH_CHECK("kv_kernel level 0");
+  LLSA_MARK(mk, "bwd_kv_fine", s);
 
   const CoarsePlan P = coarse_plan(g, units, drow_bytes);
   AdjointLevels A{};
@@ -550,6 +554,7 @@ static llsa_status bwd_impl(const Geometry& g, uint32_t units, const void* d_out
     count_launch();
     LLSA_LAUNCH_CHECK("adjoint_kernel");
   }
+  LLSA_MARK(mk, "bwd_kv_coarse", s);
   return LLSA_OK;
 }
 
@@ -559,13 +564,13 @@ llsa_status simt_backward(const Geometry& g, uint32_t units, llsa_dtype dt,
                           const void* v, const float* pyr_k, const float* pyr_v,
                           const uint32_t* tables, const uint32_t* csc_offsets,
                           const uint32_t* csc_flat, float* dq, float* dk, float* dv,
-                          void* ws, cudaStream_t s) {
+                          void* ws, cudaStream_t s, StageMarker* mk) {
   if (g.d > 256) return fail(LLSA_ERR_UNSUPPORTED, "d = %u > 256", g.d);
   if (units == 0) return LLSA_OK;
   const int cols = cols_for(g.d);
 #define BWD(T, C)                                                                           \
   return bwd_impl<T, C>(g, units, d_out, out, row_max, row_denom, q, k, v, pyr_k, pyr_v,   \
-                        tables, csc_offsets, csc_flat, dq, dk, dv, ws, s)
+                        tables, csc_offsets, csc_flat, dq, dk, dv, ws, s, mk)
   if (dt == LLSA_BF16) {
     switch (cols) {
       case 1: BWD(__nv_bfloat16, 1);

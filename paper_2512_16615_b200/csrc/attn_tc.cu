@@ -8,14 +8,15 @@ size_t tc_buffer_bytes(const Geometry&, uint32_t) { return 0; }
 void tc_carve(const Geometry&, uint32_t, char*, TcBuffers*) {}
 llsa_status tc_forward(const Geometry&, uint32_t, const void*, const void*, const void*,
                        const float*, const float*, const uint32_t*, float*, float*, float*,
-                       const TcBuffers&, cudaStream_t) {
+                       const TcBuffers&, cudaStream_t, StageMarker*) {
   return fail(LLSA_ERR_UNSUPPORTED, "tensor-core path not built");
 }
 size_t tc_backward_ws_bytes(const Geometry&, uint32_t) { return 0; }
 llsa_status tc_backward(const Geometry&, uint32_t, const void*, const float*, const float*,
                         const float*, const void*, const void*, const void*, const float*,
                         const float*, const uint32_t*, const uint32_t*, const uint32_t*,
-                        float*, float*, float*, const TcBuffers&, void*, cudaStream_t) {
+                        float*, float*, float*, const TcBuffers&, void*, cudaStream_t,
+                        StageMarker*) {
   return fail(LLSA_ERR_UNSUPPORTED, "tensor-core path not built");
 }
 

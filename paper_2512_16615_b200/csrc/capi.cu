@@ -538,8 +538,47 @@ llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units, llsa_dtype 
 // ---------------------------------------------------------------------------
 // Handle (fused) API
 // ---------------------------------------------------------------------------
+// Records named CUDA events between stages of one phase (forward or
+// backward) of a handle call; read back by llsa_handle_stage_times.
+// A ring of kRounds calls is kept so the stage times can be averaged over a
+// whole timed region without any synchronisation inside it.
+struct EventMarker final : StageMarker {
+  static constexpr int kMax = 24, kRounds = 64;
+  cudaEvent_t ev[kRounds][kMax] = {};
+  int cnt[kRounds] = {};
+  const char* name[kMax] = {};
+  int round = -1, rounds = 0;
+  bool ready = false;
+  bool init() {
+    for (int r = 0; r < kRounds; ++r)
+      for (int i = 0; i < kMax; ++i)
+        if (cudaEventCreate(&ev[r][i]) != cudaSuccess) return false;
+    ready = true;
+    return true;
+  }
+  ~EventMarker() override {
+    if (ready)
+      for (int r = 0; r < kRounds; ++r)
+        for (int i = 0; i < kMax; ++i) cudaEventDestroy(ev[r][i]);
+  }
+  void start(cudaStream_t s) {
+    round = (round + 1) % kRounds;
+    if (rounds < kRounds) ++rounds;
+    cnt[round] = 0;
+    mark("start", s);
+  }
+  void mark(const char* n, cudaStream_t s) override {
+    int& c = cnt[round];
+    if (c < kMax) {
+      name[c] = n;
+      cudaEventRecord(ev[round][c++], s);
+    }
+  }
+};
+
 struct llsa_handle_s {
   Geometry g;
+  EventMarker* timers[2] = {nullptr, nullptr};  // forward, backward
   uint32_t units = 0;
   llsa_dtype dt = LLSA_BF16;
   bool tc = false;
@@ -613,6 +652,8 @@ llsa_status llsa_handle_create(const llsa_config* cfg, uint32_t units, llsa_dtyp
 
 llsa_status llsa_handle_destroy(llsa_handle h) {
   if (!h) return LLSA_OK;
+  delete h->timers[0];
+  delete h->timers[1];
   if (h->arena) cudaFree(h->arena);
   delete h;
   return LLSA_OK;
@@ -630,17 +671,23 @@ llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, con
   const Geometry& g = h->g;
   cudaStream_t s = S(stream);
   take_launch_count();
+  EventMarker* mk = h->timers[0];
+  if (mk) mk->start(s);
   llsa_status st = pyramid(g, h->units, q, h->dt, h->pyr_q, s);
   if (!st) st = pyramid(g, h->units, k, h->dt, h->pyr_k, s);
   if (!st) st = pyramid(g, h->units, v, h->dt, h->pyr_v, s);
+  LLSA_MARK(mk, "compress", s);
   if (!st) st = hier_topk(g, h->units, h->pyr_q, h->pyr_k, h->tables, s);
+  LLSA_MARK(mk, "select", s);
   if (!st) {
-    if (h->tc)
+    if (h->tc) {
       st = tc_forward(g, h->units, q, k, v, h->pyr_k, h->pyr_v, h->tables, out, h->row_max,
-                      h->row_denom, h->tcb, s);
-    else
+                      h->row_denom, h->tcb, s, mk);
+    } else {
       st = simt_forward(g, h->units, h->dt, q, k, v, h->pyr_k, h->pyr_v, h->tables, out,
                         h->row_max, h->row_denom, s);
+      LLSA_MARK(mk, "fwd_attention", s);
+    }
   }
   h->last_launches = take_launch_count();
   return st;
@@ -661,17 +708,20 @@ llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q
   const Geometry& g = h->g;
   cudaStream_t s = S(stream);
   take_launch_count();
+  EventMarker* mk = h->timers[1];
+  if (mk) mk->start(s);
   llsa_status st = transpose_all_impl(g, h->units, h->tables, h->csc_off, h->csc_flat,
                                       h->tr_ws, s);
+  LLSA_MARK(mk, "transpose", s);
   if (!st) {
     if (h->tc)
       st = tc_backward(g, h->units, d_out, out, h->row_max, h->row_denom, q, k, v, h->pyr_k,
                        h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv, h->tcb,
-                       h->bwd_ws, s);
+                       h->bwd_ws, s, mk);
     else
       st = simt_backward(g, h->units, h->dt, d_out, out, h->row_max, h->row_denom, q, k, v,
                          h->pyr_k, h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv,
-                         h->bwd_ws, s);
+                         h->bwd_ws, s, mk);
   }
   h->last_launches = take_launch_count();
   return st;
@@ -689,5 +739,46 @@ llsa_status llsa_handle_buffer(llsa_handle h, llsa_buffer which, void** ptr, siz
 }
 
 uint32_t llsa_handle_last_launches(llsa_handle h) { return h ? h->last_launches : 0; }
+
+llsa_status llsa_handle_enable_timing(llsa_handle h, int enable) {
+  NONNULL(h);
+  for (int i = 0; i < 2; ++i) {
+    delete h->timers[i];
+    h->timers[i] = nullptr;
+    if (enable) {
+      h->timers[i] = new EventMarker();
+      if (!h->timers[i]->init()) return fail(LLSA_ERR_CUDA, "cudaEventCreate failed");
+    }
+  }
+  return LLSA_OK;
+}
+
+uint32_t llsa_handle_stage_times(llsa_handle h, const char** names, float* ms, uint32_t cap) {
+  if (!h) return 0;
+  uint32_t k = 0;
+  for (int i = 0; i < 2; ++i) {
+    EventMarker* m = h->timers[i];
+    if (!m || m->rounds == 0) continue;
+    const int n = m->cnt[m->round];
+    for (int j = 1; j < n; ++j) {
+      if (k >= cap) return k;
+      double sum = 0.0;
+      int used = 0;
+      for (int r = 0; r < m->rounds; ++r) {
+        if (m->cnt[r] != n) continue;
+        float t = 0.f;
+        if (cudaEventSynchronize(m->ev[r][j]) != cudaSuccess ||
+            cudaEventElapsedTime(&t, m->ev[r][j - 1], m->ev[r][j]) != cudaSuccess)
+          continue;
+        sum += t;
+        ++used;
+      }
+      if (names) names[k] = m->name[j];
+      if (ms) ms[k] = used ? (float)(sum / used) : -1.f;
+      ++k;
+    }
+  }
+  return k;
+}
 
 }  // extern "C"

@@ -49,6 +49,17 @@ llsa_status cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::llsa_impl::cuda_fail(_e, what);   \
   } while (0)
 
+// Optional stage-boundary recorder (handle timing): records an event on the
+// stream after a named group of launches.
+struct StageMarker {
+  virtual void mark(const char* name, cudaStream_t s) = 0;
+  virtual ~StageMarker() = default;
+};
+#define LLSA_MARK(mk, name, s) \
+  do {                         \
+    if (mk) (mk)->mark(name, s); \
+  } while (0)
+
 // Per-device sticky error word (allocated lazily).
 uint32_t* device_flag();
 
@@ -96,6 +107,6 @@ llsa_status simt_backward(const Geometry& g, uint32_t units, llsa_dtype dt,
                           const void* v, const float* pyr_k, const float* pyr_v,
                           const uint32_t* tables, const uint32_t* csc_offsets,
                           const uint32_t* csc_flat, float* dq, float* dk, float* dv,
-                          void* ws, cudaStream_t s);
+                          void* ws, cudaStream_t s, StageMarker* mk = nullptr);
 
 }  // namespace llsa_impl

@@ -25,13 +25,14 @@ void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out);
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,
-                       const TcBuffers& tb, cudaStream_t s);
+                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk = nullptr);
 size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units);
 llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                         const float* out, const float* row_max, const float* row_denom,
                         const void* q, const void* k, const void* v, const float* pyr_k,
                         const float* pyr_v, const uint32_t* tables,
                         const uint32_t* csc_offsets, const uint32_t* csc_flat, float* dq,
-                        float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s);
+                        float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s,
+                        StageMarker* mk = nullptr);
 
 }  // namespace llsa_impl

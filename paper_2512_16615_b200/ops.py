@@ -452,6 +452,17 @@ class LLSAHandle:
     def last_launches(self) -> int:
         return int(self.lib.llsa_handle_last_launches(self._h))
 
+    def enable_timing(self, on: bool = True) -> None:
+        check(self.lib.llsa_handle_enable_timing(self._h, 1 if on else 0))
+
+    def stage_times(self) -> list[tuple[str, float]]:
+        """(stage, ms) of the last forward then backward (synchronises)."""
+        cap = 48
+        names = (C.c_char_p * cap)()
+        ms = (C.c_float * cap)()
+        k = int(self.lib.llsa_handle_stage_times(self._h, names, ms, cap))
+        return [(names[i].decode(), float(ms[i])) for i in range(k)]
+
     def buffer(self, name: str) -> tuple[int, int]:
         p, b = C.c_void_p(), C.c_size_t()
         check(self.lib.llsa_handle_buffer(self._h, _lib.BUFFERS[name], C.byref(p), C.byref(b)))
