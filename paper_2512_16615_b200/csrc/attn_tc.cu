@@ -1,23 +1,1045 @@
-// Tensor-core attention (placeholder until the sm_100a kernels land).
+// Tensor-core LLSA attention for d = 64, B = 16, bf16 inputs (the BASELINE
+// shapes).  Replaces P/src/attention.cpp:145-219 (forward) and
+// P/src/attention_grad.cpp:16-265 (backward).
+//
+// Tiling follows the structure of the enriched KV set:
+//   * A CTA owns 128 consecutive queries = 8 fine query blocks, one per warp.
+//     All 8 share the same coarse entries (levels 1..L: per_level[l] row
+//     i/B^l and the full coarsest level), so the coarse keys are staged once
+//     per CTA in shared memory (double-buffered 64-key chunks, cp.async) and
+//     consumed by every warp as dense m16n8k16 tiles.
+//   * Each warp's own fine part (its K gathered level-0 blocks, each a
+//     contiguous 2 KB run of K and of V) streams through a per-warp
+//     double buffer.  The 16-query fine block is exactly one m16 MMA tile.
+//   * Online softmax in fp32 (exp2 domain), P rounded to bf16 for PV.
+//   * Coarse keys/values are the fp32 pyramid pre-scaled by the level gain
+//     (ScaleKV: B^l) and split into bf16 hi + lo (SURVEY.md hard part 3):
+//     S and dP use hi + lo (two MMAs), PV and dQ use hi.
+// Backward (mask-free, Alg. 2 of the paper):
+//   * dq kernel: query-major, same tiling; recomputes P from the saved
+//     (row_max, row_denom), dP = dO V'^T, dS = P∘(dP − D) with D = rowsum(dO∘O)
+//     from the fp32 forward output; writes dq, D and log2-LSE.
+//   * kv kernels: key-major; one warp owns one 16-key block (the m16 tile)
+//     and streams the queries that selected it (CSC segment × span, or all
+//     queries for the coarsest level) in 16-query chunks; dK', dV' stay in
+//     registers — no atomics.  Coarse levels split long query lists into
+//     fixed slices reduced in a fixed order; the fine kernel then adds the
+//     pooling adjoint of every coarse level and writes dk, dv once.
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
 #include "tc.h"
+#include "tc_common.cuh"
 
 namespace llsa_impl {
+namespace {
 
-bool tc_supported(const Geometry&, llsa_dtype) { return false; }
-size_t tc_buffer_bytes(const Geometry&, uint32_t) { return 0; }
-void tc_carve(const Geometry&, uint32_t, char*, TcBuffers*) {}
-llsa_status tc_forward(const Geometry&, uint32_t, const void*, const void*, const void*,
-                       const float*, const float*, const uint32_t*, float*, float*, float*,
-                       const TcBuffers&, cudaStream_t, StageMarker*) {
-  return fail(LLSA_ERR_UNSUPPORTED, "tensor-core path not built");
+using namespace llsa_tc;
+using bf16 = __nv_bfloat16;
+
+constexpr int kD = 64;
+constexpr int kBS = 16;
+constexpr int kTileQ = 128;
+constexpr int kMaxCoarse = 64;  // coarse entries per tile (64 × 16 = 1024 keys)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kTileBytes16 = kBS * 128;  // one 16-row swizzled tile
+
+struct TcParams {
+  const bf16 *q, *k, *v, *dout;
+  const bf16 *khi, *klo, *vhi, *vlo;  // [units][pyr_rows][64] (coarse levels)
+  const uint32_t* tables;
+  const uint32_t *csc_off, *csc_flat;
+  const float* out_in;                 // forward output (backward input)
+  float *out, *row_max, *row_denom;    // forward outputs
+  const float *rm_in, *rd_in;          // saved statistics (backward)
+  float *lse2, *drow;                  // [units][n] backward scratch
+  float *dq, *dk, *dv;
+  float* part;                         // coarse dK'/dV' partials
+  uint32_t* flag;
+  uint64_t n, pyr_rows, table_entries, csc_off_entries, csc_flat_entries;
+  uint32_t K, L, Le, lim, nce;
+  float scale;
+  uint64_t pow[kMaxLevels + 2];
+  uint64_t pyr_off[kMaxLevels + 2];
+  uint64_t table_off[kMaxLevels + 1];
+  uint64_t csc_off_off[kMaxLevels + 1], csc_flat_off[kMaxLevels + 1];
+  float bias2[kMaxLevels + 2];  // per-level logit bias × log2e (LogitBias)
+  // coarse-level partial layout (kv kernels)
+  uint32_t ncl;                          // number of coarse level slots
+  uint32_t cl_level[kMaxLevels + 2];
+  uint32_t cl_split[kMaxLevels + 2];
+  uint64_t cl_tasks[kMaxLevels + 2];     // task prefix (coarse launch)
+  uint64_t cl_part_off[kMaxLevels + 2];  // float offset of slot (per unit)
+  float cl_ck[kMaxLevels + 2], cl_cv[kMaxLevels + 2];
+  uint64_t part_unit_stride;             // floats per unit (dk + dv)
+};
+
+// Coarse entry e of the tile whose first fine block is fb0 → (level, first
+// pyramid row), canonical plan order (attention.cpp:107-118).
+__device__ __forceinline__ void coarse_entry(const TcParams& p, const uint32_t* tab,
+                                             uint64_t fb0, uint32_t e, uint32_t& lvl,
+                                             uint32_t& row) {
+  const uint32_t ksel = p.K * (p.lim - 1);
+  uint32_t b;
+  if (e < ksel) {
+    lvl = 1 + e / p.K;
+    const uint64_t r = fb0 / p.pow[lvl];
+    b = tab[p.table_off[lvl] + r * p.K + e % p.K];
+  } else {
+    lvl = p.L;
+    b = e - ksel;
+  }
+  const uint64_t blocks = p.n / p.pow[lvl + 1];
+  if (b >= blocks) {
+    raise_flag(p.flag, llsa_dev::kErrIndex);
+    b = 0;
+  }
+  row = (uint32_t)(p.pyr_off[lvl] + (uint64_t)b * kBS);
 }
-size_t tc_backward_ws_bytes(const Geometry&, uint32_t) { return 0; }
-llsa_status tc_backward(const Geometry&, uint32_t, const void*, const float*, const float*,
-                        const float*, const void*, const void*, const void*, const float*,
-                        const float*, const uint32_t*, const uint32_t*, const uint32_t*,
-                        float*, float*, float*, const TcBuffers&, void*, cudaStream_t,
-                        StageMarker*) {
-  return fail(LLSA_ERR_UNSUPPORTED, "tensor-core path not built");
+
+// ---------------------------------------------------------------------------
+// prep: coarse K'/V' = gain_l · pyramid, split into bf16 hi + lo
+// ---------------------------------------------------------------------------
+__global__ void prep_kernel(const float* __restrict__ pk, const float* __restrict__ pv,
+                            bf16* khi, bf16* klo, bf16* vhi, bf16* vlo, uint64_t pyr_rows,
+                            uint32_t units, float g1, float g2, float g3, float g4, uint64_t o2,
+                            uint64_t o3, uint64_t o4) {
+  const uint64_t total = (uint64_t)units * pyr_rows * kD;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = (i / kD) % pyr_rows;  // level of the row from its offset
+    const float g = row >= o4 ? g4 : row >= o3 ? g3 : row >= o2 ? g2 : g1;
+    const float a = pk[i] * g, b = pv[i] * g;
+    const bf16 ah = __float2bfloat16_rn(a), bh = __float2bfloat16_rn(b);
+    khi[i] = ah;
+    klo[i] = __float2bfloat16_rn(a - __bfloat162float(ah));
+    vhi[i] = bh;
+    vlo[i] = __float2bfloat16_rn(b - __bfloat162float(bh));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+struct SoftmaxState {
+  float o[8][4];
+  float m[2], l[2];
+};
+
+// Attends the warp's 16 queries (qf) to `ne` 16-key entries whose K'/V'
+// tiles start at rows e*16 of kHi/kLo/vHi.  Online softmax in log2 units.
+template <bool HILO>
+__device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t vHi, int ne,
+                                           const float* bias2, float c,
+                                           const uint32_t (&qf)[4][4], uint32_t lane,
+                                           SoftmaxState& st) {
+  float s[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[j][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (e < ne) {
+        uint32_t b[4];
+        ldb(kHi, e * 16, ks, lane, b);
+        mma16816(s[2 * e], qf[ks], b[0], b[1]);
+        mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
+        if (HILO) {
+          ldb(kLo, e * 16, ks, lane, b);
+          mma16816(s[2 * e], qf[ks], b[0], b[1]);
+          mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
+        }
+      }
+    }
+  }
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (e < ne) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float* x = s[2 * e + h];
+        x[0] = x[0] * c + bias2[e];
+        x[1] = x[1] * c + bias2[e];
+        x[2] = x[2] * c + bias2[e];
+        x[3] = x[3] * c + bias2[e];
+        mx0 = fmaxf(mx0, fmaxf(x[0], x[1]));
+        mx1 = fmaxf(mx1, fmaxf(x[2], x[3]));
+      }
+    }
+  }
+  mx0 = quad_max(mx0);
+  mx1 = quad_max(mx1);
+  const float mn0 = fmaxf(st.m[0], mx0), mn1 = fmaxf(st.m[1], mx1);
+  const float a0 = ex2(st.m[0] - mn0), a1 = ex2(st.m[1] - mn1);
+  st.m[0] = mn0;
+  st.m[1] = mn1;
+  st.l[0] *= a0;
+  st.l[1] *= a1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    st.o[j][0] *= a0;
+    st.o[j][1] *= a0;
+    st.o[j][2] *= a1;
+    st.o[j][3] *= a1;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (e < ne) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float* x = s[2 * e + h];
+        x[0] = ex2(x[0] - mn0);
+        x[1] = ex2(x[1] - mn0);
+        x[2] = ex2(x[2] - mn1);
+        x[3] = ex2(x[3] - mn1);
+        st.l[0] += x[0] + x[1];
+        st.l[1] += x[2] + x[3];
+      }
+      uint32_t a[4] = {pack_bf16(s[2 * e][0], s[2 * e][1]), pack_bf16(s[2 * e][2], s[2 * e][3]),
+                       pack_bf16(s[2 * e + 1][0], s[2 * e + 1][1]),
+                       pack_bf16(s[2 * e + 1][2], s[2 * e + 1][3])};
+#pragma unroll
+      for (int dn = 0; dn < 4; ++dn) {
+        uint32_t b[4];
+        ldb_t(vHi, e * 16, dn * 16, lane, b);
+        mma16816(st.o[2 * dn], a, b[0], b[1]);
+        mma16816(st.o[2 * dn + 1], a, b[2], b[3]);
+      }
+    }
+  }
+}
+
+// smem layout (bytes)
+constexpr int kFwdQ = kTileQ * 128;               // 16 KB
+constexpr int kFwdCStage = 3 * 64 * 128;          // Khi, Klo, V: 24 KB
+constexpr int kFwdFStage = 2 * kTileBytes16;      // K, V of one fine block: 4 KB
+constexpr int kFwdSmem = kFwdQ + 2 * kFwdCStage + 8 * 2 * kFwdFStage + 2 * kMaxCoarse * 4;
+
+__device__ __forceinline__ void load_coarse_chunk(const TcParams& p, uint32_t stage_base,
+                                                  const uint32_t* ce_row, uint32_t e0,
+                                                  uint32_t ne, const bf16* const* arrays,
+                                                  int narr, uint64_t unit_off, uint32_t tid) {
+  // entry e → rows ce_row[e0+e] .. +15 of each array; one 16 B chunk per thread-iteration
+  const uint32_t per_arr = ne * 128;  // 16 B chunks per array
+  for (uint32_t i = tid; i < per_arr * narr; i += blockDim.x) {
+    const uint32_t a = i / per_arr, r = i % per_arr;
+    const uint32_t e = r >> 7, w = r & 127;  // w: chunk within the entry's 2 KB
+    const uint32_t row = w >> 3, ch = w & 7;
+    const char* src = reinterpret_cast<const char*>(arrays[a] + unit_off +
+                                                    (uint64_t)ce_row[e0 + e] * kD) + w * 16;
+    cp_async16(stage_base + a * 8192 + swz(e * 16 + row, ch), src);
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t unit = blockIdx.y;
+  const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
+  const uint64_t fb0 = q0 / kBS;
+  const uint64_t fb = fb0 + warp;
+  const uint32_t sQ = smem_u32(smem);
+  const uint32_t sC = sQ + kFwdQ;
+  const uint32_t sF = sC + 2 * kFwdCStage + warp * 2 * kFwdFStage;
+  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + kFwdQ + 2 * kFwdCStage + 16 * kFwdFStage);
+  uint32_t* ce_lvl = ce_row + kMaxCoarse;
+
+  const uint64_t in_off = (uint64_t)unit * p.n * kD;
+  const uint64_t pyr_off = (uint64_t)unit * p.pyr_rows * kD;
+  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries;
+  const bf16* coarse[3] = {p.khi, p.klo, p.vhi};
+
+  for (uint32_t e = tid; e < p.nce; e += blockDim.x) {
+    uint32_t l, r;
+    coarse_entry(p, tab, fb0, e, l, r);
+    ce_row[e] = r;
+    ce_lvl[e] = l;
+  }
+  // fine selection of this warp (level-0 table row fb)
+  const uint32_t* frow = tab + p.table_off[0] + fb * p.K;
+  const uint64_t nfb = p.n / kBS;
+  auto fine_block = [&](uint32_t j) -> uint32_t {
+    uint32_t b = frow[j];
+    if (b >= nfb) {
+      raise_flag(p.flag, llsa_dev::kErrIndex);
+      b = 0;
+    }
+    return b;
+  };
+  auto load_fine = [&](uint32_t j, uint32_t stage) {
+    const uint32_t b = fine_block(j);
+    const uint32_t base = sF + stage * kFwdFStage;
+    load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+    load_rows_async(base + kTileBytes16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+  };
+  __syncthreads();  // ce_row visible
+
+  // group 0: Q tile, first fine block of every warp, coarse chunk 0
+  load_rows_async(sQ, 0, p.q + in_off + q0 * kD, kTileQ, tid, blockDim.x);
+  if (p.K > 0) load_fine(0, 0);
+  const uint32_t nchunks = (p.nce + 3) / 4;
+  if (nchunks) load_coarse_chunk(p, sC, ce_row, 0, min(4u, p.nce), coarse, 3, pyr_off, tid);
+  cp_async_commit();
+
+  SoftmaxState st;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) st.o[j][i] = 0.f;
+  st.m[0] = st.m[1] = -INFINITY;
+  st.l[0] = st.l[1] = 0.f;
+  const float c = p.scale * kLog2e;
+
+  uint32_t qf[4][4];
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) lda(sQ, warp * 16, ks, lane, qf[ks]);
+
+  // ---- coarse part: CTA-shared chunks of up to 4 entries (64 keys) ----
+  for (uint32_t ch = 0; ch < nchunks; ++ch) {
+    const uint32_t stage = sC + (ch & 1) * kFwdCStage;
+    if (ch + 1 < nchunks) {
+      const uint32_t e0 = (ch + 1) * 4;
+      load_coarse_chunk(p, sC + ((ch + 1) & 1) * kFwdCStage, ce_row, e0, min(4u, p.nce - e0),
+                        coarse, 3, pyr_off, tid);
+    }
+    cp_async_commit();
+    if (ch > 0) {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
+    const uint32_t e0 = ch * 4;
+    const int ne = (int)min(4u, p.nce - e0);
+    float b2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) b2[e] = e < ne ? p.bias2[ce_lvl[e0 + e]] : 0.f;
+    attend_fwd<true>(stage, stage + 8192, stage + 16384, ne, b2, c, qf, lane, st);
+    __syncthreads();  // stage may be overwritten by the next prefetch
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+
+  // ---- fine part: this warp's K gathered level-0 blocks ----
+  const float b2f[4] = {p.bias2[0], 0.f, 0.f, 0.f};
+  for (uint32_t j = 0; j < p.K; ++j) {
+    if (j + 1 < p.K) load_fine(j + 1, (j + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint32_t base = sF + (j & 1) * kFwdFStage;
+    attend_fwd<false>(base, base, base + kTileBytes16, 1, b2f, c, qf, lane, st);
+    __syncwarp();
+  }
+
+  // ---- epilogue: O = acc / l; (row_max, row_denom) in natural-log units ----
+  const float l0 = quad_sum(st.l[0]), l1 = quad_sum(st.l[1]);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
+  const uint64_t t0 = q0 + warp * 16 + r, t1 = t0 + 8;
+  float* o0 = p.out + in_off + t0 * kD;
+  float* o1 = p.out + in_off + t1 * kD;
+  bool bad = !(l0 > 0.f) || !(l1 > 0.f) || !isfinite(l0) || !isfinite(l1);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 v0 = make_float2(st.o[j][0] * i0, st.o[j][1] * i0);
+    const float2 v1 = make_float2(st.o[j][2] * i1, st.o[j][3] * i1);
+    bad |= !isfinite(v0.x) || !isfinite(v0.y) || !isfinite(v1.x) || !isfinite(v1.y);
+    *reinterpret_cast<float2*>(o0 + j * 8 + cc) = v0;
+    *reinterpret_cast<float2*>(o1 + j * 8 + cc) = v1;
+  }
+  if ((lane & 3) == 0) {
+    const uint64_t ro = (uint64_t)unit * p.n;
+    p.row_max[ro + t0] = st.m[0] / kLog2e;
+    p.row_max[ro + t1] = st.m[1] / kLog2e;
+    p.row_denom[ro + t0] = l0;
+    p.row_denom[ro + t1] = l1;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) raise_flag(p.flag, llsa_dev::kErrNonFinite);
+}
+
+// ---------------------------------------------------------------------------
+// backward: dq (query-major)
+// ---------------------------------------------------------------------------
+template <bool HILO>
+__device__ __forceinline__ void attend_dq(uint32_t kHi, uint32_t kLo, uint32_t vHi,
+                                          uint32_t vLo, int ne, const float* bias2, float c,
+                                          const uint32_t (&qf)[4][4],
+                                          const uint32_t (&gf)[4][4], float lse0, float lse1,
+                                          float D0, float D1, uint32_t lane,
+                                          float (&dq)[8][4]) {
+  float s[8][4], dp[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[j][i] = dp[j][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (e < ne) {
+        uint32_t b[4];
+        ldb(kHi, e * 16, ks, lane, b);
+        mma16816(s[2 * e], qf[ks], b[0], b[1]);
+        mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
+        ldb(vHi, e * 16, ks, lane, b);
+        mma16816(dp[2 * e], gf[ks], b[0], b[1]);
+        mma16816(dp[2 * e + 1], gf[ks], b[2], b[3]);
+        if (HILO) {
+          ldb(kLo, e * 16, ks, lane, b);
+          mma16816(s[2 * e], qf[ks], b[0], b[1]);
+          mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
+          ldb(vLo, e * 16, ks, lane, b);
+          mma16816(dp[2 * e], gf[ks], b[0], b[1]);
+          mma16816(dp[2 * e + 1], gf[ks], b[2], b[3]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (e < ne) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float* x = s[2 * e + h];
+        const float* g = dp[2 * e + h];
+        x[0] = ex2(x[0] * c + bias2[e] - lse0) * (g[0] - D0);
+        x[1] = ex2(x[1] * c + bias2[e] - lse0) * (g[1] - D0);
+        x[2] = ex2(x[2] * c + bias2[e] - lse1) * (g[2] - D1);
+        x[3] = ex2(x[3] * c + bias2[e] - lse1) * (g[3] - D1);
+      }
+      uint32_t a[4] = {pack_bf16(s[2 * e][0], s[2 * e][1]), pack_bf16(s[2 * e][2], s[2 * e][3]),
+                       pack_bf16(s[2 * e + 1][0], s[2 * e + 1][1]),
+                       pack_bf16(s[2 * e + 1][2], s[2 * e + 1][3])};
+#pragma unroll
+      for (int dn = 0; dn < 4; ++dn) {
+        uint32_t b[4];
+        ldb_t(kHi, e * 16, dn * 16, lane, b);
+        mma16816(dq[2 * dn], a, b[0], b[1]);
+        mma16816(dq[2 * dn + 1], a, b[2], b[3]);
+      }
+    }
+  }
+}
+
+constexpr int kDqQ = kTileQ * 128;          // Q tile 16 KB
+constexpr int kDqCStage = 4 * 64 * 128;     // Khi, Klo, Vhi, Vlo: 32 KB
+constexpr int kDqFStage = 2 * kTileBytes16;  // K, V: 4 KB
+constexpr int kDqSmem = 2 * kDqQ + 2 * kDqCStage + 8 * 2 * kDqFStage + 2 * kMaxCoarse * 4;
+
+__global__ void __launch_bounds__(256, 1) tc_dq_kernel(TcParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t unit = blockIdx.y;
+  const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
+  const uint64_t fb0 = q0 / kBS;
+  const uint64_t fb = fb0 + warp;
+  const uint32_t sQ = smem_u32(smem);
+  const uint32_t sG = sQ + kDqQ;
+  const uint32_t sC = sG + kDqQ;
+  const uint32_t sF = sC + 2 * kDqCStage + warp * 2 * kDqFStage;
+  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + 2 * kDqQ + 2 * kDqCStage + 16 * kDqFStage);
+  uint32_t* ce_lvl = ce_row + kMaxCoarse;
+
+  const uint64_t in_off = (uint64_t)unit * p.n * kD;
+  const uint64_t pyr_off = (uint64_t)unit * p.pyr_rows * kD;
+  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries;
+  const bf16* coarse[4] = {p.khi, p.klo, p.vhi, p.vlo};
+
+  for (uint32_t e = tid; e < p.nce; e += blockDim.x) {
+    uint32_t l, r;
+    coarse_entry(p, tab, fb0, e, l, r);
+    ce_row[e] = r;
+    ce_lvl[e] = l;
+  }
+  const uint32_t* frow = tab + p.table_off[0] + fb * p.K;
+  const uint64_t nfb = p.n / kBS;
+  auto load_fine = [&](uint32_t j, uint32_t stage) {
+    uint32_t b = frow[j];
+    if (b >= nfb) b = 0;
+    const uint32_t base = sF + stage * kDqFStage;
+    load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+    load_rows_async(base + kTileBytes16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+  };
+  __syncthreads();
+
+  load_rows_async(sQ, 0, p.q + in_off + q0 * kD, kTileQ, tid, blockDim.x);
+  load_rows_async(sG, 0, p.dout + in_off + q0 * kD, kTileQ, tid, blockDim.x);
+  if (p.K > 0) load_fine(0, 0);
+  const uint32_t nchunks = (p.nce + 3) / 4;
+  if (nchunks) load_coarse_chunk(p, sC, ce_row, 0, min(4u, p.nce), coarse, 4, pyr_off, tid);
+  cp_async_commit();
+
+  // D_t = rowsum(dO ∘ O) from the fp32 output (attention_grad.cpp:16-25) and
+  // the log2 LSE, for this warp's 16 rows; lane pair (2ρ, 2ρ+1) owns row ρ.
+  const uint32_t rr = lane >> 1, half = lane & 1;
+  const uint64_t trow = q0 + warp * 16 + rr;
+  float dsum = 0.f;
+  {
+    const float4* o4 = reinterpret_cast<const float4*>(p.out_in + in_off + trow * kD + half * 32);
+    const uint4* g4 = reinterpret_cast<const uint4*>(p.dout + in_off + trow * kD + half * 32);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 g = g4[i];
+      const float4 oa = o4[2 * i], ob = o4[2 * i + 1];
+      const uint32_t w[4] = {g.x, g.y, g.z, g.w};
+      const float of[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        dsum = fmaf(__uint_as_float(w[k] << 16), of[2 * k], dsum);
+        dsum = fmaf(__uint_as_float(w[k] & 0xffff0000u), of[2 * k + 1], dsum);
+      }
+    }
+  }
+  dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+  const uint64_t ro = (uint64_t)unit * p.n;
+  const float lse_r = p.rm_in[ro + trow] * kLog2e + __log2f(p.rd_in[ro + trow]);
+  if (half == 0) {
+    p.drow[ro + trow] = dsum;
+    p.lse2[ro + trow] = lse_r;
+  }
+  const uint32_t r = lane >> 2;
+  const float D0 = __shfl_sync(0xffffffffu, dsum, 2 * r);
+  const float D1 = __shfl_sync(0xffffffffu, dsum, 2 * (r + 8));
+  const float lse0 = __shfl_sync(0xffffffffu, lse_r, 2 * r);
+  const float lse1 = __shfl_sync(0xffffffffu, lse_r, 2 * (r + 8));
+
+  float dq[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dq[j][i] = 0.f;
+  const float c = p.scale * kLog2e;
+
+  uint32_t qf[4][4], gf[4][4];
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    lda(sQ, warp * 16, ks, lane, qf[ks]);
+    lda(sG, warp * 16, ks, lane, gf[ks]);
+  }
+
+  for (uint32_t ch = 0; ch < nchunks; ++ch) {
+    const uint32_t stage = sC + (ch & 1) * kDqCStage;
+    if (ch + 1 < nchunks) {
+      const uint32_t e0 = (ch + 1) * 4;
+      load_coarse_chunk(p, sC + ((ch + 1) & 1) * kDqCStage, ce_row, e0, min(4u, p.nce - e0),
+                        coarse, 4, pyr_off, tid);
+    }
+    cp_async_commit();
+    if (ch > 0) {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
+    const uint32_t e0 = ch * 4;
+    const int ne = (int)min(4u, p.nce - e0);
+    float b2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) b2[e] = e < ne ? p.bias2[ce_lvl[e0 + e]] : 0.f;
+    attend_dq<true>(stage, stage + 8192, stage + 16384, stage + 24576, ne, b2, c, qf, gf, lse0,
+                    lse1, D0, D1, lane, dq);
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+
+  const float b2f[4] = {p.bias2[0], 0.f, 0.f, 0.f};
+  for (uint32_t j = 0; j < p.K; ++j) {
+    if (j + 1 < p.K) load_fine(j + 1, (j + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint32_t base = sF + (j & 1) * kDqFStage;
+    attend_dq<false>(base, base, base + kTileBytes16, base + kTileBytes16, 1, b2f, c, qf, gf,
+                     lse0, lse1, D0, D1, lane, dq);
+    __syncwarp();
+  }
+
+  const uint32_t cc = (lane & 3) * 2;
+  const uint64_t t0 = q0 + warp * 16 + r, t1 = t0 + 8;
+  float* d0 = p.dq + in_off + t0 * kD;
+  float* d1 = p.dq + in_off + t1 * kD;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    *reinterpret_cast<float2*>(d0 + j * 8 + cc) =
+        make_float2(dq[j][0] * p.scale, dq[j][1] * p.scale);
+    *reinterpret_cast<float2*>(d1 + j * 8 + cc) =
+        make_float2(dq[j][2] * p.scale, dq[j][3] * p.scale);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward: dK/dV (key-major, one 16-key block per warp)
+// ---------------------------------------------------------------------------
+constexpr int kKvWarps = 4;
+constexpr int kKvKeyTiles = 4 * kTileBytes16;            // Khi, Klo, Vhi, Vlo: 8 KB
+constexpr int kKvQStage = 2 * kTileBytes16 + 2 * 16 * 4;  // Q, dO, lse2[16], D[16]
+constexpr int kKvWarpSmem = kKvKeyTiles + 2 * kKvQStage;
+constexpr int kKvSmem = kKvWarps * kKvWarpSmem;
+
+template <bool COARSE>
+__global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64_t tasks_per_unit,
+                                                              uint32_t units) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t)blockIdx.x * kKvWarps + warp;
+  const uint32_t unit = (uint32_t)(gw / tasks_per_unit);
+  uint64_t task = gw % tasks_per_unit;
+  if (unit >= units) return;  // tail warps of the last CTA
+  uint8_t* wbase = smem + warp * kKvWarpSmem;
+  const uint32_t sK = smem_u32(wbase);
+  const uint32_t sQs = sK + kKvKeyTiles;
+
+  // decode (level, key block, split)
+  uint32_t level, slot = 0, split = 0, nsplit = 1;
+  uint64_t blk;
+  if (COARSE) {
+    while (slot + 1 < p.ncl && task >= p.cl_tasks[slot + 1]) ++slot;
+    task -= p.cl_tasks[slot];
+    level = p.cl_level[slot];
+    nsplit = p.cl_split[slot];
+    blk = task / nsplit;
+    split = (uint32_t)(task % nsplit);
+  } else {
+    level = 0;
+    blk = task;
+  }
+
+  const uint64_t in_off = (uint64_t)unit * p.n * kD;
+  const uint64_t pyr_off = (uint64_t)unit * p.pyr_rows * kD;
+  const bool top = COARSE && level == p.L && p.Le == p.L;
+  const uint64_t span = top ? p.n : p.pow[level + 1];
+
+  // query list: CSC segment rows × span, or all queries for the coarsest level
+  const uint32_t* seg = nullptr;
+  uint64_t seg_len = 1;
+  if (!top) {
+    const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[level];
+    seg = p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[level] + off[blk];
+    seg_len = off[blk + 1] - off[blk];
+  }
+  const uint64_t cpr = span / 16;  // 16-query chunks per row
+  const uint64_t total = seg_len * cpr;
+  const uint64_t c_lo = total * split / nsplit, c_hi = total * (split + 1) / nsplit;
+
+  // key block tiles (A operands): level 0 → inputs; coarse → K'/V' hi, lo
+  if (COARSE) {
+    const uint64_t row0 = p.pyr_off[level] + blk * kBS;
+    load_rows_async(sK, 0, p.khi + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + kTileBytes16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + 2 * kTileBytes16, 0, p.vhi + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + 3 * kTileBytes16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
+  } else {
+    load_rows_async(sK, 0, p.k + in_off + blk * kBS * kD, kBS, lane, 32);
+    load_rows_async(sK + 2 * kTileBytes16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
+  }
+  const uint64_t ro = (uint64_t)unit * p.n;
+  auto chunk_t0 = [&](uint64_t cidx) -> uint64_t {
+    const uint64_t row = top ? 0 : seg[cidx / cpr];
+    return row * span + (cidx % cpr) * 16;
+  };
+  auto load_chunk = [&](uint64_t cidx, uint32_t stage) {
+    const uint64_t t0 = chunk_t0(cidx);
+    const uint32_t base = sQs + stage * kKvQStage;
+    load_rows_async(base, 0, p.q + in_off + t0 * kD, 16, lane, 32);
+    load_rows_async(base + kTileBytes16, 0, p.dout + in_off + t0 * kD, 16, lane, 32);
+    if (lane < 4) cp_async16(base + 2 * kTileBytes16 + lane * 16, p.lse2 + ro + t0 + lane * 4);
+    else if (lane < 8)
+      cp_async16(base + 2 * kTileBytes16 + 64 + (lane - 4) * 16, p.drow + ro + t0 + (lane - 4) * 4);
+  };
+  if (c_lo < c_hi) load_chunk(c_lo, 0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+
+  uint32_t kf[4][4], kl[4][4], vf[4][4], vl[4][4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    lda(sK, 0, ks, lane, kf[ks]);
+    lda(sK + 2 * kTileBytes16, 0, ks, lane, vf[ks]);
+    if (COARSE) {
+      lda(sK + kTileBytes16, 0, ks, lane, kl[ks]);
+      lda(sK + 3 * kTileBytes16, 0, ks, lane, vl[ks]);
+    }
+  }
+  float dk[8][4], dv[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dk[j][i] = dv[j][i] = 0.f;
+  const float c = p.scale * kLog2e;
+  const float bias = p.bias2[level];
+  const uint32_t cc = (lane & 3) * 2;
+
+  for (uint64_t ci = c_lo; ci < c_hi; ++ci) {
+    const uint32_t st = (uint32_t)((ci - c_lo) & 1);
+    if (ci + 1 < c_hi) load_chunk(ci + 1, st ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint32_t sq = sQs + st * kKvQStage;
+    const uint32_t sg = sq + kTileBytes16;
+    const float* lse = reinterpret_cast<const float*>(wbase + kKvKeyTiles + st * kKvQStage +
+                                                      2 * kTileBytes16);
+    const float* Dq = lse + 16;
+    float s[2][4], g[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[j][i] = g[j][i] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t b[4];
+      ldb(sq, 0, ks, lane, b);  // Q rows as B (k = d, n = query)
+      mma16816(s[0], kf[ks], b[0], b[1]);
+      mma16816(s[1], kf[ks], b[2], b[3]);
+      if (COARSE) {
+        mma16816(s[0], kl[ks], b[0], b[1]);
+        mma16816(s[1], kl[ks], b[2], b[3]);
+      }
+      ldb(sg, 0, ks, lane, b);  // dO rows as B
+      mma16816(g[0], vf[ks], b[0], b[1]);
+      mma16816(g[1], vf[ks], b[2], b[3]);
+      if (COARSE) {
+        mma16816(g[0], vl[ks], b[0], b[1]);
+        mma16816(g[1], vl[ks], b[2], b[3]);
+      }
+    }
+    // P^T, dS^T: element (key row, query col = nt*8 + cc + i%2)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const float la = lse[nt * 8 + cc], lb = lse[nt * 8 + cc + 1];
+      const float da = Dq[nt * 8 + cc], db = Dq[nt * 8 + cc + 1];
+      const float p0 = ex2(s[nt][0] * c + bias - la), p1 = ex2(s[nt][1] * c + bias - lb);
+      const float p2 = ex2(s[nt][2] * c + bias - la), p3 = ex2(s[nt][3] * c + bias - lb);
+      s[nt][0] = p0;
+      s[nt][1] = p1;
+      s[nt][2] = p2;
+      s[nt][3] = p3;
+      g[nt][0] = p0 * (g[nt][0] - da);
+      g[nt][1] = p1 * (g[nt][1] - db);
+      g[nt][2] = p2 * (g[nt][2] - da);
+      g[nt][3] = p3 * (g[nt][3] - db);
+    }
+    const uint32_t ap[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]),
+                            pack_bf16(s[1][0], s[1][1]), pack_bf16(s[1][2], s[1][3])};
+    const uint32_t as[4] = {pack_bf16(g[0][0], g[0][1]), pack_bf16(g[0][2], g[0][3]),
+                            pack_bf16(g[1][0], g[1][1]), pack_bf16(g[1][2], g[1][3])};
+#pragma unroll
+    for (int dn = 0; dn < 4; ++dn) {
+      uint32_t b[4];
+      ldb_t(sg, 0, dn * 16, lane, b);  // dO as [k = query][n = d]
+      mma16816(dv[2 * dn], ap, b[0], b[1]);
+      mma16816(dv[2 * dn + 1], ap, b[2], b[3]);
+      ldb_t(sq, 0, dn * 16, lane, b);  // Q as [k = query][n = d]
+      mma16816(dk[2 * dn], as, b[0], b[1]);
+      mma16816(dk[2 * dn + 1], as, b[2], b[3]);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+
+  const uint32_t r = lane >> 2;
+  if (COARSE) {
+    // raw partial sums for (slot, split): [split][token][64]
+    const uint64_t tok_l = p.n / p.pow[level];
+    float* pk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[slot] +
+                (uint64_t)split * tok_l * kD;
+    float* pv = pk + (uint64_t)nsplit * tok_l * kD;
+    const uint64_t k0 = blk * kBS + r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      *reinterpret_cast<float2*>(pk + k0 * kD + j * 8 + cc) = make_float2(dk[j][0], dk[j][1]);
+      *reinterpret_cast<float2*>(pk + (k0 + 8) * kD + j * 8 + cc) =
+          make_float2(dk[j][2], dk[j][3]);
+      *reinterpret_cast<float2*>(pv + k0 * kD + j * 8 + cc) = make_float2(dv[j][0], dv[j][1]);
+      *reinterpret_cast<float2*>(pv + (k0 + 8) * kD + j * 8 + cc) =
+          make_float2(dv[j][2], dv[j][3]);
+    }
+  } else {
+    // level 0: scale, add every coarse level's pooled-adjoint contribution
+    // (already reduced and scaled into split 0 of its slot), write once.
+    const uint64_t t0 = blk * kBS + r, t1 = t0 + 8;
+    float ak0[8][2], ak1[8][2], av0[8][2], av1[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ak0[j][0] = dk[j][0] * p.scale;
+      ak0[j][1] = dk[j][1] * p.scale;
+      ak1[j][0] = dk[j][2] * p.scale;
+      ak1[j][1] = dk[j][3] * p.scale;
+      av0[j][0] = dv[j][0];
+      av0[j][1] = dv[j][1];
+      av1[j][0] = dv[j][2];
+      av1[j][1] = dv[j][3];
+    }
+    for (uint32_t sl = 0; sl < p.ncl; ++sl) {
+      const uint32_t l = p.cl_level[sl];
+      const uint64_t tok_l = p.n / p.pow[l];
+      const float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
+      const float* gv = gk + (uint64_t)p.cl_split[sl] * tok_l * kD;
+      const uint64_t u0 = t0 / p.pow[l], u1 = t1 / p.pow[l];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 k0 = *reinterpret_cast<const float2*>(gk + u0 * kD + j * 8 + cc);
+        const float2 k1 = *reinterpret_cast<const float2*>(gk + u1 * kD + j * 8 + cc);
+        const float2 v0 = *reinterpret_cast<const float2*>(gv + u0 * kD + j * 8 + cc);
+        const float2 v1 = *reinterpret_cast<const float2*>(gv + u1 * kD + j * 8 + cc);
+        ak0[j][0] += k0.x;
+        ak0[j][1] += k0.y;
+        ak1[j][0] += k1.x;
+        ak1[j][1] += k1.y;
+        av0[j][0] += v0.x;
+        av0[j][1] += v0.y;
+        av1[j][0] += v1.x;
+        av1[j][1] += v1.y;
+      }
+    }
+    float* dk0 = p.dk + in_off + t0 * kD;
+    float* dk1 = p.dk + in_off + t1 * kD;
+    float* dv0 = p.dv + in_off + t0 * kD;
+    float* dv1 = p.dv + in_off + t1 * kD;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      *reinterpret_cast<float2*>(dk0 + j * 8 + cc) = make_float2(ak0[j][0], ak0[j][1]);
+      *reinterpret_cast<float2*>(dk1 + j * 8 + cc) = make_float2(ak1[j][0], ak1[j][1]);
+      *reinterpret_cast<float2*>(dv0 + j * 8 + cc) = make_float2(av0[j][0], av0[j][1]);
+      *reinterpret_cast<float2*>(dv1 + j * 8 + cc) = make_float2(av1[j][0], av1[j][1]);
+    }
+  }
+}
+
+// split 0 of every coarse slot ← coefficient · Σ_splits (fixed order)
+__global__ void reduce_parts_kernel(TcParams p, uint32_t units) {
+  for (uint32_t sl = 0; sl < p.ncl; ++sl) {
+    const uint64_t tok = p.n / p.pow[p.cl_level[sl]];
+    const uint64_t elems = tok * kD;
+    const uint32_t ns = p.cl_split[sl];
+    const uint64_t total = elems * units * 2;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t u = x / (2 * elems), rem = x % (2 * elems);
+      const uint32_t which = (uint32_t)(rem / elems);  // 0: dk, 1: dv
+      const uint64_t e = rem % elems;
+      float* base = p.part + u * p.part_unit_stride + p.cl_part_off[sl] +
+                    (uint64_t)which * ns * elems + e;
+      float s = 0.f;
+      for (uint32_t i = 0; i < ns; ++i) s += base[(uint64_t)i * elems];
+      base[0] = s * (which ? p.cl_cv[sl] : p.cl_ck[sl]);
+    }
+  }
+}
+
+unsigned grid_for(uint64_t threads, int block) {
+  uint64_t blocks = (threads + block - 1) / block;
+  const uint64_t cap = 148ull * 16;
+  return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
+}
+
+uint32_t coarse_entries(const Geometry& g) {
+  return g.K * (g.enrich_lim() - 1) + (g.Le == g.L ? (uint32_t)g.level_blocks(g.L) : 0u);
+}
+
+// Coarse kv slots: levels 1..lim-1, then the coarsest when L_e = L.
+void coarse_slots(const Geometry& g, TcParams& P) {
+  P.ncl = 0;
+  uint64_t tasks = 0, off = 0;
+  auto add = [&](uint32_t l, uint64_t avg_queries, uint64_t blocks) {
+    const uint32_t i = P.ncl++;
+    uint64_t s = avg_queries / 2048;
+    s = s < 1 ? 1 : s > 256 ? 256 : s;
+    P.cl_level[i] = l;
+    P.cl_split[i] = (uint32_t)s;
+    P.cl_tasks[i] = tasks;
+    tasks += blocks * s;
+    P.cl_part_off[i] = off;
+    off += 2 * s * g.level_tokens(l) * kD;
+    const float gain = g.mode == 0 ? (float)g.pow[l] : 1.f;
+    P.cl_ck[i] = g.scale * gain / (float)g.pow[l];
+    P.cl_cv[i] = gain / (float)g.pow[l];
+  };
+  for (uint32_t l = 1; l < g.enrich_lim(); ++l)
+    add(l, (uint64_t)g.K * g.pow[l + 1], g.level_blocks(l));
+  if (g.Le == g.L) add(g.L, g.n, g.level_blocks(g.L));
+  P.cl_tasks[P.ncl] = tasks;
+  P.part_unit_stride = off;
+}
+
+TcParams make_params(const Geometry& g) {
+  TcParams P{};
+  P.n = g.n;
+  P.pyr_rows = g.pyr_rows;
+  P.table_entries = g.table_entries;
+  P.csc_off_entries = g.csc_off_entries;
+  P.csc_flat_entries = g.csc_flat_entries;
+  P.K = g.K;
+  P.L = g.L;
+  P.Le = g.Le;
+  P.lim = g.enrich_lim();
+  P.nce = coarse_entries(g);
+  P.scale = g.scale;
+  for (int l = 0; l < kMaxLevels + 2; ++l) {
+    P.pow[l] = g.pow[l];
+    P.pyr_off[l] = g.pyr_off[l];
+    P.bias2[l] = g.mode == 1 && g.pow[l] ? std::log((float)g.pow[l]) * kLog2e : 0.f;
+  }
+  for (int l = 0; l < kMaxLevels + 1; ++l) {
+    P.table_off[l] = g.table_off[l];
+    P.csc_off_off[l] = g.csc_off_off[l];
+    P.csc_flat_off[l] = g.csc_flat_off[l];
+  }
+  P.flag = device_flag();
+  coarse_slots(g, P);
+  return P;
+}
+
+}  // namespace
+
+bool tc_supported(const Geometry& g, llsa_dtype dt) {
+  return dt == LLSA_BF16 && g.d == 64 && g.B == 16 && g.safe && g.n % kTileQ == 0 &&
+         g.L >= 1 && g.L <= 4 && coarse_entries(g) <= (uint32_t)kMaxCoarse;
+}
+
+size_t tc_buffer_bytes(const Geometry& g, uint32_t units) {
+  const size_t a = ((size_t)units * g.pyr_rows * kD * 2 + 255) & ~size_t(255);
+  return 4 * a;
+}
+
+void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out) {
+  const size_t a = ((size_t)units * g.pyr_rows * kD * 2 + 255) & ~size_t(255);
+  out->k_hi = reinterpret_cast<bf16*>(base);
+  out->k_lo = reinterpret_cast<bf16*>(base + a);
+  out->v_hi = reinterpret_cast<bf16*>(base + 2 * a);
+  out->v_lo = reinterpret_cast<bf16*>(base + 3 * a);
+}
+
+static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* pk,
+                               const float* pv, const TcBuffers& tb, cudaStream_t s) {
+  float gl[5] = {1, 1, 1, 1, 1};
+  uint64_t off[5] = {0, 0, ~0ull, ~0ull, ~0ull};
+  for (uint32_t l = 1; l <= g.L && l <= 4; ++l) {
+    gl[l] = g.mode == 0 ? (float)g.pow[l] : 1.f;
+    off[l] = g.pyr_off[l];
+  }
+  const uint64_t total = (uint64_t)units * g.pyr_rows * kD;
+  prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+      pk, pv, tb.k_hi, tb.k_lo, tb.v_hi, tb.v_lo, g.pyr_rows, units, gl[1], gl[2], gl[3],
+      gl[4], g.L >= 2 ? off[2] : ~0ull, g.L >= 3 ? off[3] : ~0ull, g.L >= 4 ? off[4] : ~0ull);
+  count_launch();
+  LLSA_LAUNCH_CHECK("prep_kernel");
+  return LLSA_OK;
+}
+
+llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
+                       const void* v, const float* pyr_k, const float* pyr_v,
+                       const uint32_t* tables, float* out, float* row_max, float* row_denom,
+                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk) {
+  if (llsa_status st = launch_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
+  LLSA_MARK(mk, "fwd_prep", s);
+  TcParams P = make_params(g);
+  P.q = static_cast<const bf16*>(q);
+  P.k = static_cast<const bf16*>(k);
+  P.v = static_cast<const bf16*>(v);
+  P.khi = tb.k_hi;
+  P.klo = tb.k_lo;
+  P.vhi = tb.v_hi;
+  P.vlo = tb.v_lo;
+  P.tables = tables;
+  P.out = out;
+  P.row_max = row_max;
+  P.row_denom = row_denom;
+  static bool attr = false;
+  if (!attr) {
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFwdSmem));
+    attr = true;
+  }
+  tc_fwd_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kFwdSmem, s>>>(P);
+  count_launch();
+  LLSA_LAUNCH_CHECK("tc_fwd_kernel");
+  LLSA_MARK(mk, "fwd_attention", s);
+  return LLSA_OK;
+}
+
+size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units) {
+  TcParams P{};
+  coarse_slots(g, P);
+  const size_t rows = ((size_t)units * g.n * 4 + 255) & ~size_t(255);
+  return 2 * rows + (size_t)units * P.part_unit_stride * 4 + 256;
+}
+
+llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
+                        const float* out, const float* row_max, const float* row_denom,
+                        const void* q, const void* k, const void* v, const float* pyr_k,
+                        const float* pyr_v, const uint32_t* tables,
+                        const uint32_t* csc_offsets, const uint32_t* csc_flat, float* dq,
+                        float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s,
+                        StageMarker* mk) {
+  (void)pyr_k;
+  (void)pyr_v;
+  TcParams P = make_params(g);
+  P.q = static_cast<const bf16*>(q);
+  P.k = static_cast<const bf16*>(k);
+  P.v = static_cast<const bf16*>(v);
+  P.dout = static_cast<const bf16*>(d_out);
+  P.khi = tb.k_hi;
+  P.klo = tb.k_lo;
+  P.vhi = tb.v_hi;
+  P.vlo = tb.v_lo;
+  P.tables = tables;
+  P.csc_off = csc_offsets;
+  P.csc_flat = csc_flat;
+  P.out_in = out;
+  P.rm_in = row_max;
+  P.rd_in = row_denom;
+  const size_t rows = ((size_t)units * g.n * 4 + 255) & ~size_t(255);
+  P.lse2 = static_cast<float*>(ws);
+  P.drow = reinterpret_cast<float*>(static_cast<char*>(ws) + rows);
+  P.part = reinterpret_cast<float*>(static_cast<char*>(ws) + 2 * rows);
+  P.dq = dq;
+  P.dk = dk;
+  P.dv = dv;
+  static bool attr = false;
+  if (!attr) {
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kDqSmem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+    attr = true;
+  }
+  tc_dq_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kDqSmem, s>>>(P);
+  count_launch();
+  LLSA_LAUNCH_CHECK("tc_dq_kernel");
+  LLSA_MARK(mk, "bwd_dq", s);
+  if (P.ncl) {
+    const uint64_t tasks = P.cl_tasks[P.ncl];
+    const uint64_t warps = tasks * units;
+    tc_kv_kernel<true><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32, kKvSmem,
+                         s>>>(P, tasks, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse>");
+    reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("reduce_parts_kernel");
+  }
+  LLSA_MARK(mk, "bwd_kv_coarse", s);
+  {
+    const uint64_t tasks = g.n / kBS;
+    const uint64_t warps = tasks * units;
+    tc_kv_kernel<false><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32, kKvSmem,
+                          s>>>(P, tasks, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc_kv_kernel<fine>");
+  }
+  LLSA_MARK(mk, "bwd_kv_fine", s);
+  return LLSA_OK;
 }
 
 }  // namespace llsa_impl
