@@ -6,15 +6,17 @@
 //   * A CTA owns 128 consecutive queries = 8 fine query blocks, one per warp.
 //     All 8 share the same coarse entries (levels 1..L: per_level[l] row
 //     i/B^l and the full coarsest level), so the coarse keys are staged once
-//     per CTA in shared memory (double-buffered 64-key chunks, cp.async) and
-//     consumed by every warp as dense m16n8k16 tiles.
+//     per CTA in shared memory (double-buffered chunks, cp.async) and consumed
+//     by every warp as dense m16n8k16 tiles.
 //   * Each warp's own fine part (its K gathered level-0 blocks, each a
-//     contiguous 2 KB run of K and of V) streams through a per-warp
-//     double buffer.  The 16-query fine block is exactly one m16 MMA tile.
+//     contiguous 2 KB run of K and of V) streams through a per-warp double
+//     buffer.  The 16-query fine block is exactly one m16 MMA tile.
 //   * Online softmax in fp32 (exp2 domain), P rounded to bf16 for PV.
 //   * Coarse keys/values are the fp32 pyramid pre-scaled by the level gain
 //     (ScaleKV: B^l) and split into bf16 hi + lo (SURVEY.md hard part 3):
 //     S and dP use hi + lo (two MMAs), PV and dQ use hi.
+//   * <= 112.5 KB smem and <= 128 registers per thread: 2 CTAs (16 warps) per
+//     SM, so HMMA latency is hidden across warps.
 // Backward (mask-free, Alg. 2 of the paper):
 //   * dq kernel: query-major, same tiling; recomputes P from the saved
 //     (row_max, row_denom), dP = dO V'^T, dS = P∘(dP − D) with D = rowsum(dO∘O)
@@ -43,19 +45,19 @@ constexpr int kBS = 16;
 constexpr int kTileQ = 128;
 constexpr int kMaxCoarse = 64;  // coarse entries per tile (64 × 16 = 1024 keys)
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kTileBytes16 = kBS * 128;  // one 16-row swizzled tile
+constexpr int kTile16 = kBS * 128;  // one 16-row swizzled 64-column bf16 tile
 
 struct TcParams {
   const bf16 *q, *k, *v, *dout;
   const bf16 *khi, *klo, *vhi, *vlo;  // [units][pyr_rows][64] (coarse levels)
   const uint32_t* tables;
   const uint32_t *csc_off, *csc_flat;
-  const float* out_in;                 // forward output (backward input)
-  float *out, *row_max, *row_denom;    // forward outputs
-  const float *rm_in, *rd_in;          // saved statistics (backward)
-  float *lse2, *drow;                  // [units][n] backward scratch
+  const float* out_in;               // forward output (backward input)
+  float *out, *row_max, *row_denom;  // forward outputs
+  const float *rm_in, *rd_in;        // saved statistics (backward)
+  float *lse2, *drow;                // [units][n] backward scratch
   float *dq, *dk, *dv;
-  float* part;                         // coarse dK'/dV' partials
+  float* part;  // coarse dK'/dV' partials
   uint32_t* flag;
   uint64_t n, pyr_rows, table_entries, csc_off_entries, csc_flat_entries;
   uint32_t K, L, Le, lim, nce;
@@ -66,13 +68,13 @@ struct TcParams {
   uint64_t csc_off_off[kMaxLevels + 1], csc_flat_off[kMaxLevels + 1];
   float bias2[kMaxLevels + 2];  // per-level logit bias × log2e (LogitBias)
   // coarse-level partial layout (kv kernels)
-  uint32_t ncl;                          // number of coarse level slots
+  uint32_t ncl;  // number of coarse level slots
   uint32_t cl_level[kMaxLevels + 2];
   uint32_t cl_split[kMaxLevels + 2];
   uint64_t cl_tasks[kMaxLevels + 2];     // task prefix (coarse launch)
   uint64_t cl_part_off[kMaxLevels + 2];  // float offset of slot (per unit)
   float cl_ck[kMaxLevels + 2], cl_cv[kMaxLevels + 2];
-  uint64_t part_unit_stride;             // floats per unit (dk + dv)
+  uint64_t part_unit_stride;  // floats per unit (dk + dv)
 };
 
 // Coarse entry e of the tile whose first fine block is fb0 → (level, first
@@ -96,6 +98,24 @@ __device__ __forceinline__ void coarse_entry(const TcParams& p, const uint32_t* 
     b = 0;
   }
   row = (uint32_t)(p.pyr_off[lvl] + (uint64_t)b * kBS);
+}
+
+// Copies entries e0..e0+ne-1 (16 rows each, contiguous in global) of `narr`
+// arrays into a stage whose array a starts at stage + a*arr_stride.
+__device__ __forceinline__ void load_coarse_chunk(uint32_t stage, uint32_t arr_stride,
+                                                  const uint32_t* ce_row, uint32_t e0,
+                                                  uint32_t ne, const bf16* const* arrays,
+                                                  int narr, uint64_t unit_off, uint32_t tid,
+                                                  uint32_t nthr) {
+  const uint32_t per_arr = ne * 128;  // 16 B chunks per array
+  for (uint32_t i = tid; i < per_arr * narr; i += nthr) {
+    const uint32_t a = i / per_arr, r = i % per_arr;
+    const uint32_t e = r >> 7, w = r & 127;
+    const char* src =
+        reinterpret_cast<const char*>(arrays[a] + unit_off + (uint64_t)ce_row[e0 + e] * kD) +
+        w * 16;
+    cp_async16(stage + a * arr_stride + swz(e * 16 + (w >> 3), w & 7), src);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -127,29 +147,29 @@ struct SoftmaxState {
   float m[2], l[2];
 };
 
-// Attends the warp's 16 queries (qf) to `ne` 16-key entries whose K'/V'
-// tiles start at rows e*16 of kHi/kLo/vHi.  Online softmax in log2 units.
+// Attends the warp's 16 queries (qf) to `ne` (<= 2) 16-key entries at rows
+// row0 + 16e of the K'/V' tiles.  Online softmax in log2 units.
 template <bool HILO>
-__device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t vHi, int ne,
-                                           const float* bias2, float c,
-                                           const uint32_t (&qf)[4][4], uint32_t lane,
+__device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t vHi,
+                                           uint32_t row0, int ne, float bias_a, float bias_b,
+                                           float c, const uint32_t (&qf)[4][4], uint32_t lane,
                                            SoftmaxState& st) {
-  float s[8][4];
+  float s[4][4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int i = 0; i < 4; ++i) s[j][i] = 0.f;
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 2; ++e) {
       if (e < ne) {
         uint32_t b[4];
-        ldb(kHi, e * 16, ks, lane, b);
+        ldb(kHi, row0 + e * 16, ks, lane, b);
         mma16816(s[2 * e], qf[ks], b[0], b[1]);
         mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
         if (HILO) {
-          ldb(kLo, e * 16, ks, lane, b);
+          ldb(kLo, row0 + e * 16, ks, lane, b);
           mma16816(s[2 * e], qf[ks], b[0], b[1]);
           mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
         }
@@ -158,15 +178,16 @@ __device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t 
   }
   float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 2; ++e) {
     if (e < ne) {
+      const float bias = e ? bias_b : bias_a;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float* x = s[2 * e + h];
-        x[0] = x[0] * c + bias2[e];
-        x[1] = x[1] * c + bias2[e];
-        x[2] = x[2] * c + bias2[e];
-        x[3] = x[3] * c + bias2[e];
+        x[0] = fmaf(x[0], c, bias);
+        x[1] = fmaf(x[1], c, bias);
+        x[2] = fmaf(x[2], c, bias);
+        x[3] = fmaf(x[3], c, bias);
         mx0 = fmaxf(mx0, fmaxf(x[0], x[1]));
         mx1 = fmaxf(mx1, fmaxf(x[2], x[3]));
       }
@@ -188,7 +209,7 @@ __device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t 
     st.o[j][3] *= a1;
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < 2; ++e) {
     if (e < ne) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -200,13 +221,14 @@ __device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t 
         st.l[0] += x[0] + x[1];
         st.l[1] += x[2] + x[3];
       }
-      uint32_t a[4] = {pack_bf16(s[2 * e][0], s[2 * e][1]), pack_bf16(s[2 * e][2], s[2 * e][3]),
-                       pack_bf16(s[2 * e + 1][0], s[2 * e + 1][1]),
-                       pack_bf16(s[2 * e + 1][2], s[2 * e + 1][3])};
+      const uint32_t a[4] = {pack_bf16(s[2 * e][0], s[2 * e][1]),
+                             pack_bf16(s[2 * e][2], s[2 * e][3]),
+                             pack_bf16(s[2 * e + 1][0], s[2 * e + 1][1]),
+                             pack_bf16(s[2 * e + 1][2], s[2 * e + 1][3])};
 #pragma unroll
       for (int dn = 0; dn < 4; ++dn) {
         uint32_t b[4];
-        ldb_t(vHi, e * 16, dn * 16, lane, b);
+        ldb_t(vHi, row0 + e * 16, dn * 16, lane, b);
         mma16816(st.o[2 * dn], a, b[0], b[1]);
         mma16816(st.o[2 * dn + 1], a, b[2], b[3]);
       }
@@ -214,39 +236,23 @@ __device__ __forceinline__ void attend_fwd(uint32_t kHi, uint32_t kLo, uint32_t 
   }
 }
 
-// smem layout (bytes)
-constexpr int kFwdQ = kTileQ * 128;               // 16 KB
-constexpr int kFwdCStage = 3 * 64 * 128;          // Khi, Klo, V: 24 KB
-constexpr int kFwdFStage = 2 * kTileBytes16;      // K, V of one fine block: 4 KB
-constexpr int kFwdSmem = kFwdQ + 2 * kFwdCStage + 8 * 2 * kFwdFStage + 2 * kMaxCoarse * 4;
+// smem (bytes): 2 coarse stages of 64 keys × {Khi, Klo, V} + per-warp double
+// buffer of one fine block {K, V} (its second stage first holds the warp's Q)
+constexpr int kFwdArr = 64 * 128;              // 8 KB per array per stage
+constexpr int kFwdCStage = 3 * kFwdArr;        // 24 KB
+constexpr int kFStage = 2 * kTile16;           // 4 KB
+constexpr int kFwdSmem = 2 * kFwdCStage + 8 * 2 * kFStage + 2 * kMaxCoarse * 4;  // 112.5 KB
 
-__device__ __forceinline__ void load_coarse_chunk(const TcParams& p, uint32_t stage_base,
-                                                  const uint32_t* ce_row, uint32_t e0,
-                                                  uint32_t ne, const bf16* const* arrays,
-                                                  int narr, uint64_t unit_off, uint32_t tid) {
-  // entry e → rows ce_row[e0+e] .. +15 of each array; one 16 B chunk per thread-iteration
-  const uint32_t per_arr = ne * 128;  // 16 B chunks per array
-  for (uint32_t i = tid; i < per_arr * narr; i += blockDim.x) {
-    const uint32_t a = i / per_arr, r = i % per_arr;
-    const uint32_t e = r >> 7, w = r & 127;  // w: chunk within the entry's 2 KB
-    const uint32_t row = w >> 3, ch = w & 7;
-    const char* src = reinterpret_cast<const char*>(arrays[a] + unit_off +
-                                                    (uint64_t)ce_row[e0 + e] * kD) + w * 16;
-    cp_async16(stage_base + a * 8192 + swz(e * 16 + row, ch), src);
-  }
-}
-
-__global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
+__global__ void __launch_bounds__(256, 2) tc_fwd_kernel(TcParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t unit = blockIdx.y;
   const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
   const uint64_t fb0 = q0 / kBS;
   const uint64_t fb = fb0 + warp;
-  const uint32_t sQ = smem_u32(smem);
-  const uint32_t sC = sQ + kFwdQ;
-  const uint32_t sF = sC + 2 * kFwdCStage + warp * 2 * kFwdFStage;
-  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + kFwdQ + 2 * kFwdCStage + 16 * kFwdFStage);
+  const uint32_t sC = smem_u32(smem);
+  const uint32_t sF = sC + 2 * kFwdCStage + warp * 2 * kFStage;
+  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + 2 * kFwdCStage + 16 * kFStage);
   uint32_t* ce_lvl = ce_row + kMaxCoarse;
 
   const uint64_t in_off = (uint64_t)unit * p.n * kD;
@@ -260,30 +266,26 @@ __global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
     ce_row[e] = r;
     ce_lvl[e] = l;
   }
-  // fine selection of this warp (level-0 table row fb)
   const uint32_t* frow = tab + p.table_off[0] + fb * p.K;
   const uint64_t nfb = p.n / kBS;
-  auto fine_block = [&](uint32_t j) -> uint32_t {
+  auto load_fine = [&](uint32_t j, uint32_t stage) {
     uint32_t b = frow[j];
     if (b >= nfb) {
       raise_flag(p.flag, llsa_dev::kErrIndex);
       b = 0;
     }
-    return b;
-  };
-  auto load_fine = [&](uint32_t j, uint32_t stage) {
-    const uint32_t b = fine_block(j);
-    const uint32_t base = sF + stage * kFwdFStage;
+    const uint32_t base = sF + stage * kFStage;
     load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
-    load_rows_async(base + kTileBytes16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+    load_rows_async(base + kTile16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
   };
-  __syncthreads();  // ce_row visible
+  __syncthreads();  // entry list visible
 
-  // group 0: Q tile, first fine block of every warp, coarse chunk 0
-  load_rows_async(sQ, 0, p.q + in_off + q0 * kD, kTileQ, tid, blockDim.x);
-  if (p.K > 0) load_fine(0, 0);
+  // group 0: this warp's Q rows (into fine stage 1), fine block 0, coarse chunk 0
+  load_rows_async(sF + kFStage, 0, p.q + in_off + (q0 + warp * 16) * kD, kBS, lane, 32);
+  load_fine(0, 0);
   const uint32_t nchunks = (p.nce + 3) / 4;
-  if (nchunks) load_coarse_chunk(p, sC, ce_row, 0, min(4u, p.nce), coarse, 3, pyr_off, tid);
+  if (nchunks)
+    load_coarse_chunk(sC, kFwdArr, ce_row, 0, min(4u, p.nce), coarse, 3, pyr_off, tid, 256);
   cp_async_commit();
 
   SoftmaxState st;
@@ -299,15 +301,16 @@ __global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
   cp_async_wait<0>();
   __syncthreads();
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) lda(sQ, warp * 16, ks, lane, qf[ks]);
+  for (int ks = 0; ks < 4; ++ks) lda(sF + kFStage, 0, ks, lane, qf[ks]);
+  __syncwarp();
 
   // ---- coarse part: CTA-shared chunks of up to 4 entries (64 keys) ----
   for (uint32_t ch = 0; ch < nchunks; ++ch) {
     const uint32_t stage = sC + (ch & 1) * kFwdCStage;
     if (ch + 1 < nchunks) {
       const uint32_t e0 = (ch + 1) * 4;
-      load_coarse_chunk(p, sC + ((ch + 1) & 1) * kFwdCStage, ce_row, e0, min(4u, p.nce - e0),
-                        coarse, 3, pyr_off, tid);
+      load_coarse_chunk(sC + ((ch + 1) & 1) * kFwdCStage, kFwdArr, ce_row, e0,
+                        min(4u, p.nce - e0), coarse, 3, pyr_off, tid, 256);
     }
     cp_async_commit();
     if (ch > 0) {
@@ -316,24 +319,27 @@ __global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
     }
     const uint32_t e0 = ch * 4;
     const int ne = (int)min(4u, p.nce - e0);
-    float b2[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) b2[e] = e < ne ? p.bias2[ce_lvl[e0 + e]] : 0.f;
-    attend_fwd<true>(stage, stage + 8192, stage + 16384, ne, b2, c, qf, lane, st);
+    for (int h = 0; h < ne; h += 2) {
+      const int n2 = min(2, ne - h);
+      const float ba = p.bias2[ce_lvl[e0 + h]];
+      const float bb = n2 > 1 ? p.bias2[ce_lvl[e0 + h + 1]] : 0.f;
+      attend_fwd<true>(stage, stage + kFwdArr, stage + 2 * kFwdArr, h * 16, n2, ba, bb, c, qf,
+                       lane, st);
+    }
     __syncthreads();  // stage may be overwritten by the next prefetch
   }
   cp_async_wait<0>();
   __syncwarp();
 
   // ---- fine part: this warp's K gathered level-0 blocks ----
-  const float b2f[4] = {p.bias2[0], 0.f, 0.f, 0.f};
+  const float bf = p.bias2[0];
   for (uint32_t j = 0; j < p.K; ++j) {
     if (j + 1 < p.K) load_fine(j + 1, (j + 1) & 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const uint32_t base = sF + (j & 1) * kFwdFStage;
-    attend_fwd<false>(base, base, base + kTileBytes16, 1, b2f, c, qf, lane, st);
+    const uint32_t base = sF + (j & 1) * kFStage;
+    attend_fwd<false>(base, base, base + kTile16, 0, 1, bf, bf, c, qf, lane, st);
     __syncwarp();
   }
 
@@ -366,84 +372,80 @@ __global__ void __launch_bounds__(256, 1) tc_fwd_kernel(TcParams p) {
 // ---------------------------------------------------------------------------
 // backward: dq (query-major)
 // ---------------------------------------------------------------------------
+// One 16-key entry at row0 of the K'/V' tiles: P, dP, dS, dQ += dS·K'.
 template <bool HILO>
 __device__ __forceinline__ void attend_dq(uint32_t kHi, uint32_t kLo, uint32_t vHi,
-                                          uint32_t vLo, int ne, const float* bias2, float c,
+                                          uint32_t vLo, uint32_t row0, float bias, float c,
                                           const uint32_t (&qf)[4][4],
                                           const uint32_t (&gf)[4][4], float lse0, float lse1,
                                           float D0, float D1, uint32_t lane,
                                           float (&dq)[8][4]) {
-  float s[8][4], dp[8][4];
+  float s[2][4], sl[2][4], g[2][4], gl[2][4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < 2; ++j)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) s[j][i] = dp[j][i] = 0.f;
+    for (int i = 0; i < 4; ++i) s[j][i] = sl[j][i] = g[j][i] = gl[j][i] = 0.f;
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (e < ne) {
-        uint32_t b[4];
-        ldb(kHi, e * 16, ks, lane, b);
-        mma16816(s[2 * e], qf[ks], b[0], b[1]);
-        mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
-        ldb(vHi, e * 16, ks, lane, b);
-        mma16816(dp[2 * e], gf[ks], b[0], b[1]);
-        mma16816(dp[2 * e + 1], gf[ks], b[2], b[3]);
-        if (HILO) {
-          ldb(kLo, e * 16, ks, lane, b);
-          mma16816(s[2 * e], qf[ks], b[0], b[1]);
-          mma16816(s[2 * e + 1], qf[ks], b[2], b[3]);
-          ldb(vLo, e * 16, ks, lane, b);
-          mma16816(dp[2 * e], gf[ks], b[0], b[1]);
-          mma16816(dp[2 * e + 1], gf[ks], b[2], b[3]);
-        }
-      }
+    uint32_t b[4];
+    ldb(kHi, row0, ks, lane, b);
+    mma16816(s[0], qf[ks], b[0], b[1]);
+    mma16816(s[1], qf[ks], b[2], b[3]);
+    ldb(vHi, row0, ks, lane, b);
+    mma16816(g[0], gf[ks], b[0], b[1]);
+    mma16816(g[1], gf[ks], b[2], b[3]);
+    if (HILO) {
+      ldb(kLo, row0, ks, lane, b);
+      mma16816(sl[0], qf[ks], b[0], b[1]);
+      mma16816(sl[1], qf[ks], b[2], b[3]);
+      ldb(vLo, row0, ks, lane, b);
+      mma16816(gl[0], gf[ks], b[0], b[1]);
+      mma16816(gl[1], gf[ks], b[2], b[3]);
     }
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    if (e < ne) {
+  for (int h = 0; h < 2; ++h) {
+    float* x = s[h];
+    const float* y = g[h];
+    if (HILO) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float* x = s[2 * e + h];
-        const float* g = dp[2 * e + h];
-        x[0] = ex2(x[0] * c + bias2[e] - lse0) * (g[0] - D0);
-        x[1] = ex2(x[1] * c + bias2[e] - lse0) * (g[1] - D0);
-        x[2] = ex2(x[2] * c + bias2[e] - lse1) * (g[2] - D1);
-        x[3] = ex2(x[3] * c + bias2[e] - lse1) * (g[3] - D1);
-      }
-      uint32_t a[4] = {pack_bf16(s[2 * e][0], s[2 * e][1]), pack_bf16(s[2 * e][2], s[2 * e][3]),
-                       pack_bf16(s[2 * e + 1][0], s[2 * e + 1][1]),
-                       pack_bf16(s[2 * e + 1][2], s[2 * e + 1][3])};
-#pragma unroll
-      for (int dn = 0; dn < 4; ++dn) {
-        uint32_t b[4];
-        ldb_t(kHi, e * 16, dn * 16, lane, b);
-        mma16816(dq[2 * dn], a, b[0], b[1]);
-        mma16816(dq[2 * dn + 1], a, b[2], b[3]);
+      for (int i = 0; i < 4; ++i) {
+        x[i] += sl[h][i];
+        g[h][i] += gl[h][i];
       }
     }
+    x[0] = ex2(fmaf(x[0], c, bias) - lse0) * (y[0] - D0);
+    x[1] = ex2(fmaf(x[1], c, bias) - lse0) * (y[1] - D0);
+    x[2] = ex2(fmaf(x[2], c, bias) - lse1) * (y[2] - D1);
+    x[3] = ex2(fmaf(x[3], c, bias) - lse1) * (y[3] - D1);
+  }
+  const uint32_t a[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]),
+                         pack_bf16(s[1][0], s[1][1]), pack_bf16(s[1][2], s[1][3])};
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn) {
+    uint32_t b[4];
+    ldb_t(kHi, row0, dn * 16, lane, b);
+    mma16816(dq[2 * dn], a, b[0], b[1]);
+    mma16816(dq[2 * dn + 1], a, b[2], b[3]);
   }
 }
 
-constexpr int kDqQ = kTileQ * 128;          // Q tile 16 KB
-constexpr int kDqCStage = 4 * 64 * 128;     // Khi, Klo, Vhi, Vlo: 32 KB
-constexpr int kDqFStage = 2 * kTileBytes16;  // K, V: 4 KB
-constexpr int kDqSmem = 2 * kDqQ + 2 * kDqCStage + 8 * 2 * kDqFStage + 2 * kMaxCoarse * 4;
+// smem: 2 coarse stages of 32 keys × {Khi, Klo, Vhi, Vlo} + per-warp fine
+// double buffer (stage 1 first holds the warp's Q and dO)
+constexpr int kDqArr = 32 * 128;              // 4 KB
+constexpr int kDqCStage = 4 * kDqArr;         // 16 KB
+constexpr int kDqSmem = 2 * kDqCStage + 8 * 2 * kFStage + 2 * kMaxCoarse * 4;  // 96.5 KB
 
-__global__ void __launch_bounds__(256, 1) tc_dq_kernel(TcParams p) {
+__global__ void __launch_bounds__(256, 2) tc_dq_kernel(TcParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t unit = blockIdx.y;
   const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
   const uint64_t fb0 = q0 / kBS;
   const uint64_t fb = fb0 + warp;
-  const uint32_t sQ = smem_u32(smem);
-  const uint32_t sG = sQ + kDqQ;
-  const uint32_t sC = sG + kDqQ;
-  const uint32_t sF = sC + 2 * kDqCStage + warp * 2 * kDqFStage;
-  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + 2 * kDqQ + 2 * kDqCStage + 16 * kDqFStage);
+  const uint32_t sC = smem_u32(smem);
+  const uint32_t sF = sC + 2 * kDqCStage + warp * 2 * kFStage;
+  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + 2 * kDqCStage + 16 * kFStage);
   uint32_t* ce_lvl = ce_row + kMaxCoarse;
 
   const uint64_t in_off = (uint64_t)unit * p.n * kD;
@@ -462,32 +464,34 @@ __global__ void __launch_bounds__(256, 1) tc_dq_kernel(TcParams p) {
   auto load_fine = [&](uint32_t j, uint32_t stage) {
     uint32_t b = frow[j];
     if (b >= nfb) b = 0;
-    const uint32_t base = sF + stage * kDqFStage;
+    const uint32_t base = sF + stage * kFStage;
     load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
-    load_rows_async(base + kTileBytes16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+    load_rows_async(base + kTile16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
   };
   __syncthreads();
 
-  load_rows_async(sQ, 0, p.q + in_off + q0 * kD, kTileQ, tid, blockDim.x);
-  load_rows_async(sG, 0, p.dout + in_off + q0 * kD, kTileQ, tid, blockDim.x);
-  if (p.K > 0) load_fine(0, 0);
-  const uint32_t nchunks = (p.nce + 3) / 4;
-  if (nchunks) load_coarse_chunk(p, sC, ce_row, 0, min(4u, p.nce), coarse, 4, pyr_off, tid);
+  const uint64_t qrow0 = q0 + warp * 16;
+  load_rows_async(sF + kFStage, 0, p.q + in_off + qrow0 * kD, kBS, lane, 32);
+  load_rows_async(sF + kFStage + kTile16, 0, p.dout + in_off + qrow0 * kD, kBS, lane, 32);
+  load_fine(0, 0);
+  const uint32_t nchunks = (p.nce + 1) / 2;
+  if (nchunks)
+    load_coarse_chunk(sC, kDqArr, ce_row, 0, min(2u, p.nce), coarse, 4, pyr_off, tid, 256);
   cp_async_commit();
 
   // D_t = rowsum(dO ∘ O) from the fp32 output (attention_grad.cpp:16-25) and
   // the log2 LSE, for this warp's 16 rows; lane pair (2ρ, 2ρ+1) owns row ρ.
   const uint32_t rr = lane >> 1, half = lane & 1;
-  const uint64_t trow = q0 + warp * 16 + rr;
+  const uint64_t trow = qrow0 + rr;
   float dsum = 0.f;
   {
     const float4* o4 = reinterpret_cast<const float4*>(p.out_in + in_off + trow * kD + half * 32);
     const uint4* g4 = reinterpret_cast<const uint4*>(p.dout + in_off + trow * kD + half * 32);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint4 g = g4[i];
+      const uint4 gv = g4[i];
       const float4 oa = o4[2 * i], ob = o4[2 * i + 1];
-      const uint32_t w[4] = {g.x, g.y, g.z, g.w};
+      const uint32_t w[4] = {gv.x, gv.y, gv.z, gv.w};
       const float of[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -521,48 +525,47 @@ __global__ void __launch_bounds__(256, 1) tc_dq_kernel(TcParams p) {
   __syncthreads();
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
-    lda(sQ, warp * 16, ks, lane, qf[ks]);
-    lda(sG, warp * 16, ks, lane, gf[ks]);
+    lda(sF + kFStage, 0, ks, lane, qf[ks]);
+    lda(sF + kFStage + kTile16, 0, ks, lane, gf[ks]);
   }
+  __syncwarp();
 
   for (uint32_t ch = 0; ch < nchunks; ++ch) {
     const uint32_t stage = sC + (ch & 1) * kDqCStage;
     if (ch + 1 < nchunks) {
-      const uint32_t e0 = (ch + 1) * 4;
-      load_coarse_chunk(p, sC + ((ch + 1) & 1) * kDqCStage, ce_row, e0, min(4u, p.nce - e0),
-                        coarse, 4, pyr_off, tid);
+      const uint32_t e0 = (ch + 1) * 2;
+      load_coarse_chunk(sC + ((ch + 1) & 1) * kDqCStage, kDqArr, ce_row, e0,
+                        min(2u, p.nce - e0), coarse, 4, pyr_off, tid, 256);
     }
     cp_async_commit();
     if (ch > 0) {
       cp_async_wait<1>();
       __syncthreads();
     }
-    const uint32_t e0 = ch * 4;
-    const int ne = (int)min(4u, p.nce - e0);
-    float b2[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) b2[e] = e < ne ? p.bias2[ce_lvl[e0 + e]] : 0.f;
-    attend_dq<true>(stage, stage + 8192, stage + 16384, stage + 24576, ne, b2, c, qf, gf, lse0,
-                    lse1, D0, D1, lane, dq);
+    const uint32_t e0 = ch * 2;
+    const int ne = (int)min(2u, p.nce - e0);
+    for (int e = 0; e < ne; ++e)
+      attend_dq<true>(stage, stage + kDqArr, stage + 2 * kDqArr, stage + 3 * kDqArr, e * 16,
+                      p.bias2[ce_lvl[e0 + e]], c, qf, gf, lse0, lse1, D0, D1, lane, dq);
     __syncthreads();
   }
   cp_async_wait<0>();
   __syncwarp();
 
-  const float b2f[4] = {p.bias2[0], 0.f, 0.f, 0.f};
+  const float bf = p.bias2[0];
   for (uint32_t j = 0; j < p.K; ++j) {
     if (j + 1 < p.K) load_fine(j + 1, (j + 1) & 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const uint32_t base = sF + (j & 1) * kDqFStage;
-    attend_dq<false>(base, base, base + kTileBytes16, base + kTileBytes16, 1, b2f, c, qf, gf,
-                     lse0, lse1, D0, D1, lane, dq);
+    const uint32_t base = sF + (j & 1) * kFStage;
+    attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c, qf, gf, lse0, lse1,
+                     D0, D1, lane, dq);
     __syncwarp();
   }
 
   const uint32_t cc = (lane & 3) * 2;
-  const uint64_t t0 = q0 + warp * 16 + r, t1 = t0 + 8;
+  const uint64_t t0 = qrow0 + r, t1 = t0 + 8;
   float* d0 = p.dq + in_off + t0 * kD;
   float* d1 = p.dq + in_off + t1 * kD;
 #pragma unroll
@@ -577,28 +580,39 @@ __global__ void __launch_bounds__(256, 1) tc_dq_kernel(TcParams p) {
 // ---------------------------------------------------------------------------
 // backward: dK/dV (key-major, one 16-key block per warp)
 // ---------------------------------------------------------------------------
+// Coarse levels stream 32-query chunks (rows span >= 256 queries), the fine
+// level 16-query chunks (one fine query block); 3-stage cp.async pipeline.
 constexpr int kKvWarps = 4;
-constexpr int kKvKeyTiles = 4 * kTileBytes16;            // Khi, Klo, Vhi, Vlo: 8 KB
-constexpr int kKvQStage = 2 * kTileBytes16 + 2 * 16 * 4;  // Q, dO, lse2[16], D[16]
-constexpr int kKvWarpSmem = kKvKeyTiles + 2 * kKvQStage;
-constexpr int kKvSmem = kKvWarps * kKvWarpSmem;
+constexpr int kKvKeyTiles = 4 * kTile16;  // Khi, Klo, Vhi, Vlo: 8 KB
+constexpr int kKvStages = 3;
+template <bool COARSE>
+struct KvCfg {
+  static constexpr int QC = COARSE ? 32 : 16;                 // queries per chunk
+  static constexpr int QTile = QC * 128;                      // bf16 Q (or dO) tile
+  static constexpr int Stage = 2 * QTile + 2 * QC * 4;        // Q, dO, lse2[QC], D[QC]
+  static constexpr int WarpSmem = kKvKeyTiles + kKvStages * Stage;
+  static constexpr int Smem = kKvWarps * WarpSmem;            // fine 60 KB, coarse 107 KB
+  static constexpr int MinBlocks = COARSE ? 2 : 3;
+};
 
 template <bool COARSE>
-__global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64_t tasks_per_unit,
-                                                              uint32_t units) {
+__global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
+    tc_kv_kernel(TcParams p, uint64_t tasks_per_unit, uint32_t units) {
+  using Cfg = KvCfg<COARSE>;
+  constexpr int QC = Cfg::QC, NT = QC / 8;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t gw = (uint64_t)blockIdx.x * kKvWarps + warp;
   const uint32_t unit = (uint32_t)(gw / tasks_per_unit);
   uint64_t task = gw % tasks_per_unit;
   if (unit >= units) return;  // tail warps of the last CTA
-  uint8_t* wbase = smem + warp * kKvWarpSmem;
+  uint8_t* wbase = smem + warp * Cfg::WarpSmem;
   const uint32_t sK = smem_u32(wbase);
   const uint32_t sQs = sK + kKvKeyTiles;
 
   // decode (level, key block, split)
-  uint32_t level, slot = 0, split = 0, nsplit = 1;
-  uint64_t blk;
+  uint32_t level = 0, slot = 0, split = 0, nsplit = 1;
+  uint64_t blk = task;
   if (COARSE) {
     while (slot + 1 < p.ncl && task >= p.cl_tasks[slot + 1]) ++slot;
     task -= p.cl_tasks[slot];
@@ -606,9 +620,6 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
     nsplit = p.cl_split[slot];
     blk = task / nsplit;
     split = (uint32_t)(task % nsplit);
-  } else {
-    level = 0;
-    blk = task;
   }
 
   const uint64_t in_off = (uint64_t)unit * p.n * kD;
@@ -624,7 +635,7 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
     seg = p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[level] + off[blk];
     seg_len = off[blk + 1] - off[blk];
   }
-  const uint64_t cpr = span / 16;  // 16-query chunks per row
+  const uint64_t cpr = span / QC;  // chunks per row
   const uint64_t total = seg_len * cpr;
   const uint64_t c_lo = total * split / nsplit, c_hi = total * (split + 1) / nsplit;
 
@@ -632,40 +643,43 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
   if (COARSE) {
     const uint64_t row0 = p.pyr_off[level] + blk * kBS;
     load_rows_async(sK, 0, p.khi + pyr_off + row0 * kD, kBS, lane, 32);
-    load_rows_async(sK + kTileBytes16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
-    load_rows_async(sK + 2 * kTileBytes16, 0, p.vhi + pyr_off + row0 * kD, kBS, lane, 32);
-    load_rows_async(sK + 3 * kTileBytes16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + kTile16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + 2 * kTile16, 0, p.vhi + pyr_off + row0 * kD, kBS, lane, 32);
+    load_rows_async(sK + 3 * kTile16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
   } else {
     load_rows_async(sK, 0, p.k + in_off + blk * kBS * kD, kBS, lane, 32);
-    load_rows_async(sK + 2 * kTileBytes16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
+    load_rows_async(sK + 2 * kTile16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
   }
   const uint64_t ro = (uint64_t)unit * p.n;
-  auto chunk_t0 = [&](uint64_t cidx) -> uint64_t {
-    const uint64_t row = top ? 0 : seg[cidx / cpr];
-    return row * span + (cidx % cpr) * 16;
-  };
   auto load_chunk = [&](uint64_t cidx, uint32_t stage) {
-    const uint64_t t0 = chunk_t0(cidx);
-    const uint32_t base = sQs + stage * kKvQStage;
-    load_rows_async(base, 0, p.q + in_off + t0 * kD, 16, lane, 32);
-    load_rows_async(base + kTileBytes16, 0, p.dout + in_off + t0 * kD, 16, lane, 32);
-    if (lane < 4) cp_async16(base + 2 * kTileBytes16 + lane * 16, p.lse2 + ro + t0 + lane * 4);
-    else if (lane < 8)
-      cp_async16(base + 2 * kTileBytes16 + 64 + (lane - 4) * 16, p.drow + ro + t0 + (lane - 4) * 4);
+    const uint64_t row = top ? 0 : seg[cidx / cpr];
+    const uint64_t t0 = row * span + (cidx % cpr) * QC;
+    const uint32_t base = sQs + stage * Cfg::Stage;
+    load_rows_async(base, 0, p.q + in_off + t0 * kD, QC, lane, 32);
+    load_rows_async(base + Cfg::QTile, 0, p.dout + in_off + t0 * kD, QC, lane, 32);
+    constexpr uint32_t nv = QC / 4;  // 16 B vectors of lse2 (then of D)
+    if (lane < nv)
+      cp_async16(base + 2 * Cfg::QTile + lane * 16, p.lse2 + ro + t0 + lane * 4);
+    else if (lane < 2 * nv)
+      cp_async16(base + 2 * Cfg::QTile + QC * 4 + (lane - nv) * 16,
+                 p.drow + ro + t0 + (lane - nv) * 4);
   };
-  if (c_lo < c_hi) load_chunk(c_lo, 0);
+  const uint64_t nchunk = c_hi - c_lo;
+  if (nchunk > 0) load_chunk(c_lo, 0);
   cp_async_commit();
-  cp_async_wait<0>();
+  if (nchunk > 1) load_chunk(c_lo + 1, 1);
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncwarp();
 
   uint32_t kf[4][4], kl[4][4], vf[4][4], vl[4][4];
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     lda(sK, 0, ks, lane, kf[ks]);
-    lda(sK + 2 * kTileBytes16, 0, ks, lane, vf[ks]);
+    lda(sK + 2 * kTile16, 0, ks, lane, vf[ks]);
     if (COARSE) {
-      lda(sK + kTileBytes16, 0, ks, lane, kl[ks]);
-      lda(sK + 3 * kTileBytes16, 0, ks, lane, vl[ks]);
+      lda(sK + kTile16, 0, ks, lane, kl[ks]);
+      lda(sK + 3 * kTile16, 0, ks, lane, vl[ks]);
     }
   }
   float dk[8][4], dv[8][4];
@@ -677,47 +691,51 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
   const float bias = p.bias2[level];
   const uint32_t cc = (lane & 3) * 2;
 
-  for (uint64_t ci = c_lo; ci < c_hi; ++ci) {
-    const uint32_t st = (uint32_t)((ci - c_lo) & 1);
-    if (ci + 1 < c_hi) load_chunk(ci + 1, st ^ 1);
+  for (uint64_t i = 0; i < nchunk; ++i) {
+    const uint32_t st = (uint32_t)(i % kKvStages);
+    if (i + 2 < nchunk) load_chunk(c_lo + i + 2, (uint32_t)((i + 2) % kKvStages));
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<2>();
     __syncwarp();
-    const uint32_t sq = sQs + st * kKvQStage;
-    const uint32_t sg = sq + kTileBytes16;
-    const float* lse = reinterpret_cast<const float*>(wbase + kKvKeyTiles + st * kKvQStage +
-                                                      2 * kTileBytes16);
-    const float* Dq = lse + 16;
-    float s[2][4], g[2][4];
+    const uint32_t sq = sQs + st * Cfg::Stage;
+    const uint32_t sg = sq + Cfg::QTile;
+    const float* lse =
+        reinterpret_cast<const float*>(wbase + kKvKeyTiles + st * Cfg::Stage + 2 * Cfg::QTile);
+    const float* Dq = lse + QC;
+    // S^T = K' Q^T and dP^T = V' dO^T over QC queries (NT n-tiles of 8)
+    float s[NT][4], g[NT][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) s[j][i] = g[j][i] = 0.f;
+      for (int e = 0; e < 4; ++e) s[j][e] = g[j][e] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      uint32_t b[4];
-      ldb(sq, 0, ks, lane, b);  // Q rows as B (k = d, n = query)
-      mma16816(s[0], kf[ks], b[0], b[1]);
-      mma16816(s[1], kf[ks], b[2], b[3]);
-      if (COARSE) {
-        mma16816(s[0], kl[ks], b[0], b[1]);
-        mma16816(s[1], kl[ks], b[2], b[3]);
-      }
-      ldb(sg, 0, ks, lane, b);  // dO rows as B
-      mma16816(g[0], vf[ks], b[0], b[1]);
-      mma16816(g[1], vf[ks], b[2], b[3]);
-      if (COARSE) {
-        mma16816(g[0], vl[ks], b[0], b[1]);
-        mma16816(g[1], vl[ks], b[2], b[3]);
+#pragma unroll
+      for (int h = 0; h < NT / 2; ++h) {
+        uint32_t b[4];
+        ldb(sq, h * 16, ks, lane, b);  // Q rows as B (k = d, n = query)
+        mma16816(s[2 * h], kf[ks], b[0], b[1]);
+        mma16816(s[2 * h + 1], kf[ks], b[2], b[3]);
+        if (COARSE) {
+          mma16816(s[2 * h], kl[ks], b[0], b[1]);
+          mma16816(s[2 * h + 1], kl[ks], b[2], b[3]);
+        }
+        ldb(sg, h * 16, ks, lane, b);  // dO rows as B
+        mma16816(g[2 * h], vf[ks], b[0], b[1]);
+        mma16816(g[2 * h + 1], vf[ks], b[2], b[3]);
+        if (COARSE) {
+          mma16816(g[2 * h], vl[ks], b[0], b[1]);
+          mma16816(g[2 * h + 1], vl[ks], b[2], b[3]);
+        }
       }
     }
-    // P^T, dS^T: element (key row, query col = nt*8 + cc + i%2)
+    // P^T, dS^T: element (key row, query col = nt*8 + cc + e%2)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
       const float la = lse[nt * 8 + cc], lb = lse[nt * 8 + cc + 1];
       const float da = Dq[nt * 8 + cc], db = Dq[nt * 8 + cc + 1];
-      const float p0 = ex2(s[nt][0] * c + bias - la), p1 = ex2(s[nt][1] * c + bias - lb);
-      const float p2 = ex2(s[nt][2] * c + bias - la), p3 = ex2(s[nt][3] * c + bias - lb);
+      const float p0 = ex2(fmaf(s[nt][0], c, bias) - la), p1 = ex2(fmaf(s[nt][1], c, bias) - lb);
+      const float p2 = ex2(fmaf(s[nt][2], c, bias) - la), p3 = ex2(fmaf(s[nt][3], c, bias) - lb);
       s[nt][0] = p0;
       s[nt][1] = p1;
       s[nt][2] = p2;
@@ -727,19 +745,27 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
       g[nt][2] = p2 * (g[nt][2] - da);
       g[nt][3] = p3 * (g[nt][3] - db);
     }
-    const uint32_t ap[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]),
-                            pack_bf16(s[1][0], s[1][1]), pack_bf16(s[1][2], s[1][3])};
-    const uint32_t as[4] = {pack_bf16(g[0][0], g[0][1]), pack_bf16(g[0][2], g[0][3]),
-                            pack_bf16(g[1][0], g[1][1]), pack_bf16(g[1][2], g[1][3])};
+    // dV' += P^T dO, dK' += dS^T Q: k-steps of 16 queries
 #pragma unroll
-    for (int dn = 0; dn < 4; ++dn) {
-      uint32_t b[4];
-      ldb_t(sg, 0, dn * 16, lane, b);  // dO as [k = query][n = d]
-      mma16816(dv[2 * dn], ap, b[0], b[1]);
-      mma16816(dv[2 * dn + 1], ap, b[2], b[3]);
-      ldb_t(sq, 0, dn * 16, lane, b);  // Q as [k = query][n = d]
-      mma16816(dk[2 * dn], as, b[0], b[1]);
-      mma16816(dk[2 * dn + 1], as, b[2], b[3]);
+    for (int kk = 0; kk < NT / 2; ++kk) {
+      const uint32_t ap[4] = {pack_bf16(s[2 * kk][0], s[2 * kk][1]),
+                              pack_bf16(s[2 * kk][2], s[2 * kk][3]),
+                              pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                              pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+      const uint32_t as[4] = {pack_bf16(g[2 * kk][0], g[2 * kk][1]),
+                              pack_bf16(g[2 * kk][2], g[2 * kk][3]),
+                              pack_bf16(g[2 * kk + 1][0], g[2 * kk + 1][1]),
+                              pack_bf16(g[2 * kk + 1][2], g[2 * kk + 1][3])};
+#pragma unroll
+      for (int dn = 0; dn < 4; ++dn) {
+        uint32_t b[4];
+        ldb_t(sg, kk * 16, dn * 16, lane, b);  // dO as [k = query][n = d]
+        mma16816(dv[2 * dn], ap, b[0], b[1]);
+        mma16816(dv[2 * dn + 1], ap, b[2], b[3]);
+        ldb_t(sq, kk * 16, dn * 16, lane, b);  // Q as [k = query][n = d]
+        mma16816(dk[2 * dn], as, b[0], b[1]);
+        mma16816(dk[2 * dn + 1], as, b[2], b[3]);
+      }
     }
     __syncwarp();
   }
@@ -766,17 +792,12 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
     // level 0: scale, add every coarse level's pooled-adjoint contribution
     // (already reduced and scaled into split 0 of its slot), write once.
     const uint64_t t0 = blk * kBS + r, t1 = t0 + 8;
-    float ak0[8][2], ak1[8][2], av0[8][2], av1[8][2];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      ak0[j][0] = dk[j][0] * p.scale;
-      ak0[j][1] = dk[j][1] * p.scale;
-      ak1[j][0] = dk[j][2] * p.scale;
-      ak1[j][1] = dk[j][3] * p.scale;
-      av0[j][0] = dv[j][0];
-      av0[j][1] = dv[j][1];
-      av1[j][0] = dv[j][2];
-      av1[j][1] = dv[j][3];
+      dk[j][0] *= p.scale;
+      dk[j][1] *= p.scale;
+      dk[j][2] *= p.scale;
+      dk[j][3] *= p.scale;
     }
     for (uint32_t sl = 0; sl < p.ncl; ++sl) {
       const uint32_t l = p.cl_level[sl];
@@ -790,14 +811,14 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
         const float2 k1 = *reinterpret_cast<const float2*>(gk + u1 * kD + j * 8 + cc);
         const float2 v0 = *reinterpret_cast<const float2*>(gv + u0 * kD + j * 8 + cc);
         const float2 v1 = *reinterpret_cast<const float2*>(gv + u1 * kD + j * 8 + cc);
-        ak0[j][0] += k0.x;
-        ak0[j][1] += k0.y;
-        ak1[j][0] += k1.x;
-        ak1[j][1] += k1.y;
-        av0[j][0] += v0.x;
-        av0[j][1] += v0.y;
-        av1[j][0] += v1.x;
-        av1[j][1] += v1.y;
+        dk[j][0] += k0.x;
+        dk[j][1] += k0.y;
+        dk[j][2] += k1.x;
+        dk[j][3] += k1.y;
+        dv[j][0] += v0.x;
+        dv[j][1] += v0.y;
+        dv[j][2] += v1.x;
+        dv[j][3] += v1.y;
       }
     }
     float* dk0 = p.dk + in_off + t0 * kD;
@@ -806,10 +827,10 @@ __global__ void __launch_bounds__(kKvWarps * 32) tc_kv_kernel(TcParams p, uint64
     float* dv1 = p.dv + in_off + t1 * kD;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      *reinterpret_cast<float2*>(dk0 + j * 8 + cc) = make_float2(ak0[j][0], ak0[j][1]);
-      *reinterpret_cast<float2*>(dk1 + j * 8 + cc) = make_float2(ak1[j][0], ak1[j][1]);
-      *reinterpret_cast<float2*>(dv0 + j * 8 + cc) = make_float2(av0[j][0], av0[j][1]);
-      *reinterpret_cast<float2*>(dv1 + j * 8 + cc) = make_float2(av1[j][0], av1[j][1]);
+      *reinterpret_cast<float2*>(dk0 + j * 8 + cc) = make_float2(dk[j][0], dk[j][1]);
+      *reinterpret_cast<float2*>(dk1 + j * 8 + cc) = make_float2(dk[j][2], dk[j][3]);
+      *reinterpret_cast<float2*>(dv0 + j * 8 + cc) = make_float2(dv[j][0], dv[j][1]);
+      *reinterpret_cast<float2*>(dv1 + j * 8 + cc) = make_float2(dv[j][2], dv[j][3]);
     }
   }
 }
@@ -921,15 +942,12 @@ void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out) {
 static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* pk,
                                const float* pv, const TcBuffers& tb, cudaStream_t s) {
   float gl[5] = {1, 1, 1, 1, 1};
-  uint64_t off[5] = {0, 0, ~0ull, ~0ull, ~0ull};
-  for (uint32_t l = 1; l <= g.L && l <= 4; ++l) {
-    gl[l] = g.mode == 0 ? (float)g.pow[l] : 1.f;
-    off[l] = g.pyr_off[l];
-  }
+  for (uint32_t l = 1; l <= g.L && l <= 4; ++l) gl[l] = g.mode == 0 ? (float)g.pow[l] : 1.f;
   const uint64_t total = (uint64_t)units * g.pyr_rows * kD;
   prep_kernel<<<grid_for(total, 256), 256, 0, s>>>(
       pk, pv, tb.k_hi, tb.k_lo, tb.v_hi, tb.v_lo, g.pyr_rows, units, gl[1], gl[2], gl[3],
-      gl[4], g.L >= 2 ? off[2] : ~0ull, g.L >= 3 ? off[3] : ~0ull, g.L >= 4 ? off[4] : ~0ull);
+      gl[4], g.L >= 2 ? g.pyr_off[2] : ~0ull, g.L >= 3 ? g.pyr_off[3] : ~0ull,
+      g.L >= 4 ? g.pyr_off[4] : ~0ull);
   count_launch();
   LLSA_LAUNCH_CHECK("prep_kernel");
   return LLSA_OK;
@@ -1009,9 +1027,11 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kDqSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       KvCfg<true>::Smem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       KvCfg<false>::Smem));
     attr = true;
   }
   tc_dq_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kDqSmem, s>>>(P);
@@ -1021,8 +1041,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   if (P.ncl) {
     const uint64_t tasks = P.cl_tasks[P.ncl];
     const uint64_t warps = tasks * units;
-    tc_kv_kernel<true><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32, kKvSmem,
-                         s>>>(P, tasks, units);
+    tc_kv_kernel<true><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
+                         KvCfg<true>::Smem, s>>>(P, tasks, units);
     count_launch();
     LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse>");
     reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units);
@@ -1033,8 +1053,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   {
     const uint64_t tasks = g.n / kBS;
     const uint64_t warps = tasks * units;
-    tc_kv_kernel<false><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32, kKvSmem,
-                          s>>>(P, tasks, units);
+    tc_kv_kernel<false><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
+                          KvCfg<false>::Smem, s>>>(P, tasks, units);
     count_launch();
     LLSA_LAUNCH_CHECK("tc_kv_kernel<fine>");
   }

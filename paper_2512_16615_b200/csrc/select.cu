@@ -146,6 +146,131 @@ __global__ void __launch_bounds__(256) select_level_kernel(
   }
 }
 
+// Fast variant for d % 4 == 0, B = 16 query rows per block, C = K·B <= 256
+// candidates, K <= 32: thread (row r, lane group cg) scores candidates
+// cg, cg+16, … with q_r and the candidate rows streamed as float4 from smem
+// (4 exact accumulators per pair, same association as detail::dot); then one
+// warp per row extracts the top K by K rounds of a warp arg-max over
+// (score desc, position asc) and emits the kept positions in ascending order.
+template <int CPT>
+__global__ void __launch_bounds__(256) select_level_fast_kernel(
+    const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
+    uint64_t k_unit_stride, const uint32_t* __restrict__ parent, uint64_t parent_unit_stride,
+    uint32_t parent_k, uint32_t key_blocks, uint32_t d, uint32_t K, float scale,
+    uint32_t* __restrict__ out, uint64_t out_unit_stride, uint32_t* flag) {
+  constexpr uint32_t B = 16;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t blk = blockIdx.x, unit = blockIdx.y;
+  const uint32_t C = parent_k * B;
+  const uint32_t ld = d + 4;  // padded row stride (floats), keeps 16 B alignment
+  uint32_t* ids = reinterpret_cast<uint32_t*>(smem);                  // 256
+  float* scores = reinterpret_cast<float*>(ids + 256);                // 16 × 256
+  float* sq = scores + 16 * 256;                                      // 16 × ld
+  float* sk = sq + 16 * ld;                                           // C × ld
+  const uint32_t* prow = parent + unit * parent_unit_stride + (uint64_t)blk * parent_k;
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    uint32_t pb = prow[c / B];
+    if (pb >= key_blocks) {
+      raise_flag(flag, kErrIndex);
+      pb = 0;
+    }
+    ids[c] = pb * B + c % B;
+  }
+  const float* qu = q + unit * q_unit_stride + (uint64_t)blk * B * d;
+  const uint32_t d4 = d / 4;
+  for (uint32_t e = threadIdx.x; e < B * d4; e += blockDim.x) {
+    const uint32_t r = e / d4, j = e % d4;
+    reinterpret_cast<float4*>(sq + r * ld)[j] = reinterpret_cast<const float4*>(qu + r * d)[j];
+  }
+  __syncthreads();
+  const float* ku = k + unit * k_unit_stride;
+  for (uint32_t e = threadIdx.x; e < C * d4; e += blockDim.x) {
+    const uint32_t c = e / d4, j = e % d4;
+    reinterpret_cast<float4*>(sk + c * ld)[j] =
+        __ldg(reinterpret_cast<const float4*>(ku + (uint64_t)ids[c] * d) + j);
+  }
+  __syncthreads();
+  {
+    const uint32_t r = threadIdx.x >> 4, cg = threadIdx.x & 15;
+    float acc[CPT][4];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    const float4* qr = reinterpret_cast<const float4*>(sq + r * ld);
+    for (uint32_t j = 0; j < d4; ++j) {
+      const float4 x = qr[j];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const uint32_t c = cg + 16 * i;
+        if (c < C) {
+          const float4 y = reinterpret_cast<const float4*>(sk + c * ld)[j];
+          acc[i][0] = __fadd_rn(acc[i][0], __fmul_rn(x.x, y.x));
+          acc[i][1] = __fadd_rn(acc[i][1], __fmul_rn(x.y, y.y));
+          acc[i][2] = __fadd_rn(acc[i][2], __fmul_rn(x.z, y.z));
+          acc[i][3] = __fadd_rn(acc[i][3], __fmul_rn(x.w, y.w));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      const uint32_t c = cg + 16 * i;
+      if (c < C)
+        scores[r * 256 + c] = __fmul_rn(
+            scale, __fadd_rn(__fadd_rn(acc[i][0], acc[i][1]), __fadd_rn(acc[i][2], acc[i][3])));
+    }
+  }
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t r = warp; r < B; r += blockDim.x >> 5) {
+    // lane owns positions lane*8 .. lane*8+7 (contiguous → ballot order = position order)
+    float sv[8];
+    uint32_t taken = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t c = lane * 8 + i;
+      sv[i] = c < C ? scores[r * 256 + c] : -INFINITY;
+    }
+    const uint32_t valid = lane * 8 < C ? ((C - lane * 8 >= 8) ? 0xffu : ((1u << (C - lane * 8)) - 1u)) : 0u;
+    for (uint32_t round = 0; round < K; ++round) {
+      float best = 0.f;
+      uint32_t bpos = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t c = lane * 8 + i;
+        if (((valid & ~taken) >> i) & 1u) {
+          if (bpos == 0xffffffffu || sv[i] > best) {  // positions ascend: ties keep first
+            best = sv[i];
+            bpos = c;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const uint32_t op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const bool take = op != 0xffffffffu &&
+                          (bpos == 0xffffffffu || ob > best || (ob == best && op < bpos));
+        if (take) {
+          best = ob;
+          bpos = op;
+        }
+      }
+      if (bpos / 8 == lane) taken |= 1u << (bpos % 8);
+    }
+    const uint32_t cnt = __popc(taken);
+    uint32_t pre = cnt;  // inclusive scan of counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= (uint32_t)o) pre += y;
+    }
+    uint32_t pos = pre - cnt;
+    uint32_t* o = out + unit * out_unit_stride + ((uint64_t)blk * B + r) * K;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((taken >> i) & 1u) o[pos++] = ids[lane * 8 + i];
+  }
+}
+
 }  // namespace
 
 llsa_status launch_select_coarsest(const float* q, uint64_t q_unit_stride, const float* k,
@@ -176,6 +301,23 @@ llsa_status launch_select_level(const float* q, uint64_t q_unit_stride, const fl
                                 uint32_t* out, uint64_t out_unit_stride, cudaStream_t s) {
   if (parent_rows == 0 || units == 0) return LLSA_OK;
   const uint64_t C = (uint64_t)parent_k * B;
+  if (B == 16 && d % 4 == 0 && d <= 256 && C <= 256 && K <= 32) {
+    const uint64_t ld = d + 4;
+    const size_t smem = 4 * (256 + 16 * 256 + 16 * ld + C * ld);
+    if (smem <= 200 * 1024) {
+      const uint32_t key_blocks = (uint32_t)(k_rows / B);
+      auto kern = C <= 128 ? select_level_fast_kernel<8> : select_level_fast_kernel<16>;
+      if (smem > 48 * 1024)
+        LLSA_CUDA_TRY(
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<dim3(parent_rows, units), 256, smem, s>>>(
+          q, q_unit_stride, k, k_unit_stride, parent, parent_unit_stride, parent_k, key_blocks,
+          d, K, scale, out, out_unit_stride, device_flag());
+      count_launch();
+      LLSA_LAUNCH_CHECK("select_level_fast_kernel");
+      return LLSA_OK;
+    }
+  }
   const uint64_t ld = (d + 3) & ~3u, ldk = ld + 4;
   const uint64_t base = 4 * ((C + 3) & ~3ull) + 4 * B * ld + 4 * ((B * C + 3) & ~3ull) +
                         ((B * C + 15) & ~15ull);
