@@ -169,6 +169,17 @@ llsa_status llsa_forward(const llsa_config* cfg, uint32_t units, llsa_dtype dtyp
                          const uint32_t* tables, float* out, float* row_max,
                          float* row_denom, void* stream);
 
+/* llsa_forward over a materialised EnrichedKVPlan (attention.hpp:34-41):
+ * plan_{level,block,weight} [units][n/B][entries_per_block], any entries
+ * (hand-built plans included, weights honoured as attention.cpp:176-180).
+ * The caller range-checks the plan (attention.cpp:74-76). */
+llsa_status llsa_forward_plan(const llsa_config* cfg, uint32_t units, llsa_dtype dtype,
+                              const void* q, const void* k, const void* v,
+                              const float* pyr_k, const float* pyr_v,
+                              const uint32_t* plan_level, const uint32_t* plan_block,
+                              const float* plan_weight, uint32_t entries_per_block,
+                              float* out, float* row_max, float* row_denom, void* stream);
+
 /* ---- backward ---------------------------------------------------------------- */
 size_t llsa_backward_workspace_bytes(const llsa_config* cfg, uint32_t units);
 /* llsa_backward, P/include/llsa/attention_grad.hpp:45-52
@@ -185,6 +196,17 @@ llsa_status llsa_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dty
                           const uint32_t* csc_flat, float* dq, float* dk,
                           float* dv, void* workspace, size_t workspace_bytes,
                           void* stream);
+/* llsa_backward with dq taken over a materialised plan (as the reference's
+ * query-major phase, attention_grad.cpp:229-257); dk/dv from the CSC lists. */
+llsa_status llsa_backward_plan(const llsa_config* cfg, uint32_t units, llsa_dtype dtype,
+                               const void* d_out, const float* out, const float* row_max,
+                               const float* row_denom, const void* q, const void* k,
+                               const void* v, const float* pyr_k, const float* pyr_v,
+                               const uint32_t* plan_level, const uint32_t* plan_block,
+                               const float* plan_weight, uint32_t entries_per_block,
+                               const uint32_t* csc_offsets, const uint32_t* csc_flat,
+                               float* dq, float* dk, float* dv, void* workspace,
+                               size_t workspace_bytes, void* stream);
 /* kv_backward, P/include/llsa/attention_grad.hpp:32-37 (attention_grad.cpp:90-202):
  * dk/dv only (dq not computed). */
 llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units,

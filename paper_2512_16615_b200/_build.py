@@ -77,11 +77,22 @@ def build(verbose: bool = False, force: bool = False) -> dict[str, str]:
     shim_src = sorted(glob.glob(os.path.join(CSRC, "shim", "*.cpp")))
     if shim_src and (force or _stale(SHIM_LIB, shim_src + hdrs + [CUDA_LIB])):
         _run([CXX] + CXX_FLAGS + ["-shared", "-o", SHIM_LIB] + shim_src +
-             [f"-L{OUT}", "-lllsa_cuda", f"-Wl,-rpath,$ORIGIN",
-              "-L/usr/local/cuda/lib64", "-lcudart"])
+             [f"-L{OUT}", "-lllsa_cuda", "-Wl,-rpath,$ORIGIN",
+              "-L/usr/local/cuda/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
+    # C++ parity tests of the drop-in API (tests/cpp), run by tests/test_cpp_shim.py
+    tests_cpp = os.path.join(ROOT, "tests", "cpp")
+    built_tests = []
+    for src in sorted(glob.glob(os.path.join(tests_cpp, "test_*.cpp"))):
+        exe = os.path.join(PKG, "build", "tests", os.path.basename(src)[:-4])
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        if force or _stale(exe, [src, SHIM_LIB, os.path.join(tests_cpp, "doctest.h")] + hdrs):
+            _run([CXX, "-std=c++20", "-O2", f"-I{tests_cpp}", f"-I{INCLUDE}", "-o", exe, src,
+                  f"-L{OUT}", "-lllsa", f"-Wl,-rpath,{OUT}"])
+        built_tests.append(exe)
     if verbose:
-        print(f"built {CUDA_LIB}" + (f", {SHIM_LIB}" if shim_src else ""))
-    return {"cuda": CUDA_LIB, "shim": SHIM_LIB if shim_src else ""}
+        print(f"built {CUDA_LIB}" + (f", {SHIM_LIB}" if shim_src else "") +
+              (f", {len(built_tests)} C++ test program(s)" if built_tests else ""))
+    return {"cuda": CUDA_LIB, "shim": SHIM_LIB if shim_src else "", "tests": built_tests}
 
 
 if __name__ == "__main__":

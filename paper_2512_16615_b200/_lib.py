@@ -88,6 +88,9 @@ SIGNATURES = {
     "llsa_build_plan": (C.c_int, [_cfgp, _u32, _vp, _vp, _vp, _vp, _vp]),
     "llsa_forward": (C.c_int, [_cfgp, _u32, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                _vp, _vp]),
+    "llsa_forward_plan": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 8 + [_u32] + [_vp] * 4),
+    "llsa_backward_plan": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 12 + [_u32] +
+                           [_vp] * 6 + [_sz, _vp]),
     "llsa_backward_workspace_bytes": (_sz, [_cfgp, _u32]),
     "llsa_backward": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 16 + [_sz, _vp]),
     "llsa_kv_backward": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 14 + [_sz, _vp]),

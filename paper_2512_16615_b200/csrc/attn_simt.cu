@@ -36,6 +36,12 @@ struct Dims {
   uint64_t pow[kMaxLevels + 2];
   uint64_t table_off[kMaxLevels + 1];
   uint64_t table_stride;
+  // Optional materialised plan (llsa_forward_plan / llsa_backward_plan):
+  // [units][n/B][epb] (level, block, weight); when set it replaces the tables.
+  const uint32_t* plan_level;
+  const uint32_t* plan_block;
+  const float* plan_weight;
+  uint32_t epb;
 };
 
 template <int COLS, typename T>
@@ -69,19 +75,27 @@ __device__ __forceinline__ void level_row(const Levels<T>& P, uint32_t u, uint32
   }
 }
 
-// Iterates the enriched KV entries of fine block i in canonical plan order
-// (attention.cpp:107-118), calling f(level, block).
+// Iterates the enriched KV entries of fine block i of unit u in canonical
+// plan order (attention.cpp:107-118), calling f(level, block, weight); with a
+// materialised plan the entries (and their weights) come from the plan.
 template <typename F>
-__device__ __forceinline__ void for_each_entry(const Dims& D, const uint32_t* tables_u,
-                                               uint64_t i, F&& f) {
+__device__ __forceinline__ void for_each_entry(const Dims& D, const uint32_t* tables,
+                                               uint64_t u, uint64_t i, F&& f) {
+  if (D.plan_level) {
+    const uint64_t base = (u * (D.n / D.B) + i) * D.epb;
+    for (uint32_t e = 0; e < D.epb; ++e)
+      f(D.plan_level[base + e], D.plan_block[base + e], D.plan_weight[base + e]);
+    return;
+  }
+  const uint32_t* tables_u = tables + u * D.table_stride;
   for (uint32_t l = 0; l < D.lim; ++l) {
     const uint64_t row = i / D.pow[l];
     const uint32_t* tr = tables_u + D.table_off[l] + row * D.K;
-    for (uint32_t j = 0; j < D.K; ++j) f(l, tr[j]);
+    for (uint32_t j = 0; j < D.K; ++j) f(l, tr[j], (float)D.pow[l]);
   }
   if (D.Le == D.L) {
     const uint64_t top = D.n / D.pow[D.L + 1];
-    for (uint64_t b = 0; b < top; ++b) f(D.L, (uint32_t)b);
+    for (uint64_t b = 0; b < top; ++b) f(D.L, (uint32_t)b, (float)D.pow[D.L]);
   }
 }
 
@@ -93,10 +107,10 @@ __global__ void plan_kernel(Dims D, uint32_t E, uint32_t units, const uint32_t* 
        x += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t u = x / fine, i = x - u * fine;
     uint64_t e = x * E;
-    for_each_entry(D, tables + u * D.table_stride, i, [&](uint32_t l, uint32_t b) {
+    for_each_entry(D, tables, u, i, [&](uint32_t l, uint32_t b, float w) {
       pl[e] = l;
       pb[e] = b;
-      pw[e] = (float)D.pow[l];
+      pw[e] = w;
       ++e;
     });
   }
@@ -120,9 +134,7 @@ __global__ void __launch_bounds__(256) fwd_kernel(Dims D, uint32_t units, const 
 #pragma unroll
   for (int c = 0; c < COLS; ++c) acc[c] = 0.f;
   float m = D.safe ? -INFINITY : 0.f, denom = 0.f;
-  for_each_entry(D, tables + (uint64_t)u * D.table_stride, t / B,
-                 [&](uint32_t l, uint32_t blk) {
-    const float w = (float)D.pow[l];
+  for_each_entry(D, tables, u, t / B, [&](uint32_t l, uint32_t blk, float w) {
     const float kg = scale_kv ? w : 1.f;          // attention.cpp:176-180
     const float bias = scale_kv ? 0.f : logf(w);
     for (uint32_t b = 0; b < B; ++b) {
@@ -200,9 +212,7 @@ __global__ void __launch_bounds__(256) dq_kernel(Dims D, uint32_t units, const T
 #pragma unroll
   for (int c = 0; c < COLS; ++c) acc[c] = 0.f;
   const float m = row_max[tok], inv_den = 1.f / row_denom[tok], Dt = drow[tok];
-  for_each_entry(D, tables + (uint64_t)u * D.table_stride, t / B,
-                 [&](uint32_t l, uint32_t blk) {
-    const float w = (float)D.pow[l];
+  for_each_entry(D, tables, u, t / B, [&](uint32_t l, uint32_t blk, float w) {
     const float kg = scale_kv ? w : 1.f;
     const float bias = scale_kv ? 0.f : logf(w);
     for (uint32_t b = 0; b < B; ++b) {
@@ -359,8 +369,14 @@ unsigned grid_for(uint64_t threads, int block) {
 
 unsigned warps_grid(uint64_t warps) { return (unsigned)((warps * 32 + 255) / 256); }
 
-Dims make_dims(const Geometry& g) {
+Dims make_dims(const Geometry& g, const PlanView* plan = nullptr) {
   Dims D{};
+  if (plan && plan->level) {
+    D.plan_level = plan->level;
+    D.plan_block = plan->block;
+    D.plan_weight = plan->weight;
+    D.epb = plan->epb;
+  }
   D.n = g.n;
   D.d = g.d;
   D.B = g.B;
@@ -440,29 +456,30 @@ template <typename T, int COLS>
 static void fwd_dispatch(const Geometry& g, uint32_t units, const void* q, const void* k,
                          const void* v, const float* pyr_k, const float* pyr_v,
                          const uint32_t* tables, float* out, float* rm, float* rd,
-                         cudaStream_t s) {
+                         cudaStream_t s, const PlanView* plan) {
   fwd_kernel<T, COLS><<<warps_grid(g.n * units), 256, 0, s>>>(
-      make_dims(g), units, static_cast<const T*>(q), make_levels<T>(g, k, pyr_k),
+      make_dims(g, plan), units, static_cast<const T*>(q), make_levels<T>(g, k, pyr_k),
       make_levels<T>(g, v, pyr_v), tables, out, rm, rd, device_flag());
 }
 
 llsa_status simt_forward(const Geometry& g, uint32_t units, llsa_dtype dt, const void* q,
                          const void* k, const void* v, const float* pyr_k,
                          const float* pyr_v, const uint32_t* tables, float* out,
-                         float* row_max, float* row_denom, cudaStream_t s) {
+                         float* row_max, float* row_denom, cudaStream_t s,
+                         const PlanView* plan) {
   if (g.d > 256) return fail(LLSA_ERR_UNSUPPORTED, "d = %u > 256", g.d);
   if (units == 0) return LLSA_OK;
   const int cols = cols_for(g.d);
 #define FWD(T)                                                                             \
   switch (cols) {                                                                          \
     case 1: fwd_dispatch<T, 1>(g, units, q, k, v, pyr_k, pyr_v, tables, out, row_max,      \
-                               row_denom, s); break;                                       \
+                               row_denom, s, plan); break;                                 \
     case 2: fwd_dispatch<T, 2>(g, units, q, k, v, pyr_k, pyr_v, tables, out, row_max,      \
-                               row_denom, s); break;                                       \
+                               row_denom, s, plan); break;                                 \
     case 4: fwd_dispatch<T, 4>(g, units, q, k, v, pyr_k, pyr_v, tables, out, row_max,      \
-                               row_denom, s); break;                                       \
+                               row_denom, s, plan); break;                                 \
     default: fwd_dispatch<T, 8>(g, units, q, k, v, pyr_k, pyr_v, tables, out, row_max,     \
-                                row_denom, s); break;                                      \
+                                row_denom, s, plan); break;                                \
   }
   if (dt == LLSA_BF16) {
     FWD(__nv_bfloat16)
@@ -487,13 +504,13 @@ static llsa_status bwd_impl(const Geometry& g, uint32_t units, const void* d_out
                             const float* pyr_k, const float* pyr_v, const uint32_t* tables,
                             const uint32_t* csc_offsets, const uint32_t* csc_flat,
                             float* dq, float* dk, float* dv, void* ws, cudaStream_t s,
-                            StageMarker* mk) {
+                            StageMarker* mk, const PlanView* plan) {
   const T* q = static_cast<const T*>(q_);
   const T* dout = static_cast<const T*>(d_out_);
   char* base = static_cast<char*>(ws);
   float* drow = reinterpret_cast<float*>(base);
   const uint64_t drow_bytes = (units * g.n * 4 + 255) & ~255ull;
-  const Dims D = make_dims(g);
+  const Dims D = make_dims(g, plan);
   const Levels<T> Kp = make_levels<T>(g, k, pyr_k), Vp = make_levels<T>(g, v, pyr_v);
 
   drow_kernel<T, COLS><<<warps_grid(g.n * units), 256, 0, s>>>(g.n * units, g.d, dout, out,
@@ -564,13 +581,13 @@ llsa_status simt_backward(const Geometry& g, uint32_t units, llsa_dtype dt,
                           const void* v, const float* pyr_k, const float* pyr_v,
                           const uint32_t* tables, const uint32_t* csc_offsets,
                           const uint32_t* csc_flat, float* dq, float* dk, float* dv,
-                          void* ws, cudaStream_t s, StageMarker* mk) {
+                          void* ws, cudaStream_t s, StageMarker* mk, const PlanView* plan) {
   if (g.d > 256) return fail(LLSA_ERR_UNSUPPORTED, "d = %u > 256", g.d);
   if (units == 0) return LLSA_OK;
   const int cols = cols_for(g.d);
 #define BWD(T, C)                                                                           \
   return bwd_impl<T, C>(g, units, d_out, out, row_max, row_denom, q, k, v, pyr_k, pyr_v,   \
-                        tables, csc_offsets, csc_flat, dq, dk, dv, ws, s, mk)
+                        tables, csc_offsets, csc_flat, dq, dk, dv, ws, s, mk, plan)
   if (dt == LLSA_BF16) {
     switch (cols) {
       case 1: BWD(__nv_bfloat16, 1);

@@ -469,6 +469,59 @@ llsa_status llsa_forward(const llsa_config* cfg, uint32_t units, llsa_dtype dt, 
   return simt_forward(g, units, dt, q, k, v, pyr_k, pyr_v, tables, out, rm, rd, S(stream));
 }
 
+llsa_status llsa_forward_plan(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                              const void* q, const void* k, const void* v, const float* pyr_k,
+                              const float* pyr_v, const uint32_t* pl, const uint32_t* pb,
+                              const float* pw, uint32_t epb, float* out, float* rm, float* rd,
+                              void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  if (epb && (!pl || !pb || !pw)) return fail(LLSA_ERR_ARGUMENT, "null plan");
+  PlanView plan{pl, pb, pw, epb};
+  return simt_forward(g, units, dt, q, k, v, pyr_k, pyr_v, nullptr, out, rm, rd, S(stream),
+                      &plan);
+}
+
+llsa_status llsa_backward_plan(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                               const void* d_out, const float* out, const float* rm,
+                               const float* rd, const void* q, const void* k, const void* v,
+                               const float* pyr_k, const float* pyr_v, const uint32_t* pl,
+                               const uint32_t* pb, const float* pw, uint32_t epb,
+                               const uint32_t* offs, const uint32_t* flat, float* dq,
+                               float* dk, float* dv, void* ws, size_t ws_bytes, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(d_out);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(offs);
+  NONNULL(flat);
+  NONNULL(dq);
+  NONNULL(dk);
+  NONNULL(dv);
+  if (g.L >= 1 && (!pyr_k || !pyr_v)) return fail(LLSA_ERR_ARGUMENT, "null pyramid");
+  if (epb && (!pl || !pb || !pw)) return fail(LLSA_ERR_ARGUMENT, "null plan");
+  if (!ws || ws_bytes < simt_backward_ws_bytes(g, units))
+    return fail(LLSA_ERR_ARGUMENT, "backward workspace too small");
+  PlanView plan{pl, pb, pw, epb};
+  return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, nullptr, offs,
+                       flat, dq, dk, dv, ws, S(stream), nullptr, &plan);
+}
+
 size_t llsa_backward_workspace_bytes(const llsa_config* cfg, uint32_t units) {
   Geometry g;
   if (make_geometry(cfg, &g)) return 0;

@@ -95,11 +95,21 @@ llsa_status launch_build_plan(const Geometry& g, uint32_t units, const uint32_t*
                               uint32_t* plan_level, uint32_t* plan_block,
                               float* plan_weight, cudaStream_t s);
 
+// A materialised enriched plan ([units][n/B][epb] level, block, weight):
+// hand-built plans are honoured exactly as the reference does.
+struct PlanView {
+  const uint32_t* level = nullptr;
+  const uint32_t* block = nullptr;
+  const float* weight = nullptr;
+  uint32_t epb = 0;
+};
+
 // General (SIMT) attention, any d <= 256 and any B.
 llsa_status simt_forward(const Geometry& g, uint32_t units, llsa_dtype dt, const void* q,
                          const void* k, const void* v, const float* pyr_k,
                          const float* pyr_v, const uint32_t* tables, float* out,
-                         float* row_max, float* row_denom, cudaStream_t s);
+                         float* row_max, float* row_denom, cudaStream_t s,
+                         const PlanView* plan = nullptr);
 size_t simt_backward_ws_bytes(const Geometry& g, uint32_t units);
 llsa_status simt_backward(const Geometry& g, uint32_t units, llsa_dtype dt,
                           const void* d_out, const float* out, const float* row_max,
@@ -107,6 +117,7 @@ llsa_status simt_backward(const Geometry& g, uint32_t units, llsa_dtype dt,
                           const void* v, const float* pyr_k, const float* pyr_v,
                           const uint32_t* tables, const uint32_t* csc_offsets,
                           const uint32_t* csc_flat, float* dq, float* dk, float* dv,
-                          void* ws, cudaStream_t s, StageMarker* mk = nullptr);
+                          void* ws, cudaStream_t s, StageMarker* mk = nullptr,
+                          const PlanView* plan = nullptr);
 
 }  // namespace llsa_impl
