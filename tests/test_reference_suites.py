@@ -20,8 +20,8 @@ RT = os.path.join(ROOT, "oracle", "_ref", "reftests")
 # Cases whose tolerance is double-only (fail identically in the reference's
 # own LLSA_SINGLE_PRECISION build).
 FP32_TOLERANCE_CASES = {
-    "pyramid": {"pooling matches an independent per-level reference",
-                "column sums are preserved at every level"},
+    "pyramid": {"column sums are preserved at every level",
+                "pool_backward is the adjoint of pooling"},
     "attention": {"a constant value matrix collapses the output to that constant",
                   "keeping every block reduces to dense attention",
                   "the streaming pass matches the dense two-pass reference",
@@ -30,9 +30,12 @@ FP32_TOLERANCE_CASES = {
     "attention_grad": {"with every block kept the gradient equals dense attention's",
                        "the sparse backward agrees with the dense-mask reference",
                        "the key-major pass matches its mask-driven baseline"},
-    "oracle": {"effective attention equals dense attention when everything is kept",
-               "finite differences confirm the backward pass"},
+    "oracle": {"dense attention outputs are convex combinations of the values",
+               "logit biasing has a closed form when all logits tie"},
 }
+# This set is exactly what the reference's own float build fails when the same
+# suites are linked against it (oracle/Makefile `reftests32`, recorded in
+# tests/golden/ref_f32_suite_failures.json).
 CPU_SUITES = ("core", "tensorio")
 GPU_SUITES = ("pyramid", "selection", "indexmap", "attention", "attention_grad", "oracle")
 
