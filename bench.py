@@ -194,7 +194,11 @@ def main() -> None:
     ap.add_argument("--impl", default="llsa", choices=["llsa", "reference"])
     ap.add_argument("--n", type=int, default=N_TOK)
     ap.add_argument("--levels", type=int, default=LEVELS)
-    ap.add_argument("--units", type=int, default=UNITS_PER_GPU)
+    ap.add_argument("--units", type=int, default=UNITS_PER_GPU,
+                    help="units per GPU (weak scaling, default)")
+    ap.add_argument("--global-units", type=int, default=0,
+                    help="fixed total units split over the GPUs (strong scaling, e.g. 128 "
+                         "for BASELINE C4 = batch 8 x 16 heads)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -203,12 +207,18 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2512_16615_b200.sharding import shard_units
+    scaling = "weak"
+    if args.global_units:
+        args.units = shard_units(args.global_units, world, rank)[1]
+        scaling = "strong"
     cfg_json = {"workload": f"LLSA fwd+bwd, N={args.n}, {args.units} units (batch·head) per "
                             f"GPU, d=64, B=16, K=8, L={args.levels} (BASELINE '4 levels'), "
                             "L_e=L, ScaleKV, bf16 in / fp32 out",
                 "n": args.n, "d": D, "block_size": B, "top_k": K, "levels": args.levels,
                 "enrich_levels": args.levels, "units_per_gpu": args.units,
-                "global_units": args.units * world, "parallelism": f"units/{world}gpu",
+                "global_units": args.global_units or args.units * world,
+                "parallelism": f"batch*head units sharded over {world} GPU(s), no collective",
                 "l2": "inputs larger than L2 (4 x units x N x 64 bf16 per step)"}
 
     if args.impl == "reference":
@@ -279,10 +289,8 @@ def main() -> None:
     ms = e0.elapsed_time(e1) / args.steps
     stages = h.stage_times()
     llsa.sync_status()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    from paper_2512_16615_b200.sharding import max_over_ranks
+    ms = max_over_ranks(ms)
 
     # ---- roofline of the dominant kernel (stage) ----------------------------
     peaks, peak_src = _peaks()
@@ -337,10 +345,7 @@ def main() -> None:
         torch.cuda.synchronize()
         barrier()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms)
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4 * q.numel() * 2,
                "d2h_bytes_per_step": 4 * out.numel() * 4, "steps": e2e_steps,
                "path": "llsa_handle_forward/backward (C ABI) with pinned host buffers"}
@@ -357,10 +362,10 @@ def main() -> None:
     if rank == 0:
         line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": False, "scaling": scaling, "vs_baseline": None,
                 "dtype": "bf16", "data": "synthetic (torch.randn N(0,1) -> bf16, resident in "
                 "HBM)", "config": cfg_json,
-                "units_per_s": units * world / (ms * 1e-3),
+                "units_per_s": (args.global_units or units * world) / (ms * 1e-3),
                 "effective_tflops": total_flops / (ms * 1e-3) / 1e12,
                 "ideal_ms": ideal_ms,
                 "roofline": roof,

@@ -16,3 +16,4 @@ from .ops import (ForwardState, LLSAConfig, LLSAHandle, ValidatedConfig, build_p
                   transpose_all, transpose_indices, validate_config)
 
 __all__ = [n for n in dir() if not n.startswith("__")]
+from .autograd import LLSAAttention  # noqa: E402
