@@ -480,8 +480,9 @@ def rel_err(a, ref) -> dict:
     fro = float(np.linalg.norm(diff) / (np.linalg.norm(ref) or 1.0))
     if ref.ndim == 2:
         rn = np.linalg.norm(ref, axis=1)
-        rn[rn == 0] = 1.0
-        worst_row = float((np.linalg.norm(diff, axis=1) / rn).max())
+        keep = rn > 1e-3 * max(float(rn.max()), 1e-30)   # ignore ~zero reference rows
+        worst_row = float((np.linalg.norm(diff, axis=1)[keep] / rn[keep]).max()) \
+            if keep.any() else 0.0
     else:
         worst_row = float(np.abs(diff).max() / mx)
     return {"max_rel": float(np.abs(diff).max()) / mx, "fro": fro, "worst_row": worst_row}

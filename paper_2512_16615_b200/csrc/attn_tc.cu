@@ -28,6 +28,7 @@
 //     fixed slices reduced in a fixed order; the fine kernel then adds the
 //     pooling adjoint of every coarse level and writes dk, dv once.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -67,6 +68,9 @@ struct TcParams {
   uint64_t table_off[kMaxLevels + 1];
   uint64_t csc_off_off[kMaxLevels + 1], csc_flat_off[kMaxLevels + 1];
   float bias2[kMaxLevels + 2];  // per-level logit bias × log2e (LogitBias)
+  // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
+  // shallower ones (gain B^l small) use hi only.
+  uint32_t hilo_level;
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
   uint32_t cl_level[kMaxLevels + 2];
@@ -323,8 +327,13 @@ __global__ void __launch_bounds__(256, 2) tc_fwd_kernel(TcParams p) {
       const int n2 = min(2, ne - h);
       const float ba = p.bias2[ce_lvl[e0 + h]];
       const float bb = n2 > 1 ? p.bias2[ce_lvl[e0 + h + 1]] : 0.f;
-      attend_fwd<true>(stage, stage + kFwdArr, stage + 2 * kFwdArr, h * 16, n2, ba, bb, c, qf,
-                       lane, st);
+      const uint32_t lv = max(ce_lvl[e0 + h], n2 > 1 ? ce_lvl[e0 + h + 1] : 0u);
+      if (lv >= p.hilo_level)
+        attend_fwd<true>(stage, stage + kFwdArr, stage + 2 * kFwdArr, h * 16, n2, ba, bb, c, qf,
+                         lane, st);
+      else
+        attend_fwd<false>(stage, stage + kFwdArr, stage + 2 * kFwdArr, h * 16, n2, ba, bb, c,
+                          qf, lane, st);
     }
     __syncthreads();  // stage may be overwritten by the next prefetch
   }
@@ -544,9 +553,14 @@ __global__ void __launch_bounds__(256, 2) tc_dq_kernel(TcParams p) {
     }
     const uint32_t e0 = ch * 2;
     const int ne = (int)min(2u, p.nce - e0);
-    for (int e = 0; e < ne; ++e)
-      attend_dq<true>(stage, stage + kDqArr, stage + 2 * kDqArr, stage + 3 * kDqArr, e * 16,
-                      p.bias2[ce_lvl[e0 + e]], c, qf, gf, lse0, lse1, D0, D1, lane, dq);
+    for (int e = 0; e < ne; ++e) {
+      if (ce_lvl[e0 + e] >= p.hilo_level)
+        attend_dq<true>(stage, stage + kDqArr, stage + 2 * kDqArr, stage + 3 * kDqArr, e * 16,
+                        p.bias2[ce_lvl[e0 + e]], c, qf, gf, lse0, lse1, D0, D1, lane, dq);
+      else
+        attend_dq<false>(stage, stage + kDqArr, stage + 2 * kDqArr, stage + 3 * kDqArr, e * 16,
+                         p.bias2[ce_lvl[e0 + e]], c, qf, gf, lse0, lse1, D0, D1, lane, dq);
+    }
     __syncthreads();
   }
   cp_async_wait<0>();
@@ -595,9 +609,13 @@ struct KvCfg {
   static constexpr int MinBlocks = COARSE ? 2 : 3;
 };
 
-template <bool COARSE>
-__global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
-    tc_kv_kernel(TcParams p, uint64_t tasks_per_unit, uint32_t units) {
+// MODE 0: fine level; 1: coarse levels with hi-only K'/V'; 2: coarse levels
+// with hi + lo.  A launch covers the coarse slots [slot_begin, slot_end).
+template <int MODE>
+__global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
+    tc_kv_kernel(TcParams p, uint64_t tasks_per_unit, uint32_t units, uint32_t slot_begin) {
+  constexpr bool COARSE = MODE > 0;
+  constexpr bool use_lo = MODE == 2;
   using Cfg = KvCfg<COARSE>;
   constexpr int QC = Cfg::QC, NT = QC / 8;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -611,9 +629,10 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
   const uint32_t sQs = sK + kKvKeyTiles;
 
   // decode (level, key block, split)
-  uint32_t level = 0, slot = 0, split = 0, nsplit = 1;
+  uint32_t level = 0, slot = slot_begin, split = 0, nsplit = 1;
   uint64_t blk = task;
   if (COARSE) {
+    task += p.cl_tasks[slot_begin];
     while (slot + 1 < p.ncl && task >= p.cl_tasks[slot + 1]) ++slot;
     task -= p.cl_tasks[slot];
     level = p.cl_level[slot];
@@ -643,9 +662,11 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
   if (COARSE) {
     const uint64_t row0 = p.pyr_off[level] + blk * kBS;
     load_rows_async(sK, 0, p.khi + pyr_off + row0 * kD, kBS, lane, 32);
-    load_rows_async(sK + kTile16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
     load_rows_async(sK + 2 * kTile16, 0, p.vhi + pyr_off + row0 * kD, kBS, lane, 32);
-    load_rows_async(sK + 3 * kTile16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
+    if (use_lo) {
+      load_rows_async(sK + kTile16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
+      load_rows_async(sK + 3 * kTile16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
+    }
   } else {
     load_rows_async(sK, 0, p.k + in_off + blk * kBS * kD, kBS, lane, 32);
     load_rows_async(sK + 2 * kTile16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
@@ -677,7 +698,7 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
   for (int ks = 0; ks < 4; ++ks) {
     lda(sK, 0, ks, lane, kf[ks]);
     lda(sK + 2 * kTile16, 0, ks, lane, vf[ks]);
-    if (COARSE) {
+    if (use_lo) {
       lda(sK + kTile16, 0, ks, lane, kl[ks]);
       lda(sK + 3 * kTile16, 0, ks, lane, vl[ks]);
     }
@@ -716,14 +737,14 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<COARSE>::MinBlocks)
         ldb(sq, h * 16, ks, lane, b);  // Q rows as B (k = d, n = query)
         mma16816(s[2 * h], kf[ks], b[0], b[1]);
         mma16816(s[2 * h + 1], kf[ks], b[2], b[3]);
-        if (COARSE) {
+        if (use_lo) {
           mma16816(s[2 * h], kl[ks], b[0], b[1]);
           mma16816(s[2 * h + 1], kl[ks], b[2], b[3]);
         }
         ldb(sg, h * 16, ks, lane, b);  // dO rows as B
         mma16816(g[2 * h], vf[ks], b[0], b[1]);
         mma16816(g[2 * h + 1], vf[ks], b[2], b[3]);
-        if (COARSE) {
+        if (use_lo) {
           mma16816(g[2 * h], vl[ks], b[0], b[1]);
           mma16816(g[2 * h + 1], vl[ks], b[2], b[3]);
         }
@@ -915,6 +936,8 @@ TcParams make_params(const Geometry& g) {
     P.csc_flat_off[l] = g.csc_flat_off[l];
   }
   P.flag = device_flag();
+  const char* hl = getenv("LLSA_HILO_LEVEL");  // 1: hi + lo on every coarse level
+  P.hilo_level = hl ? (uint32_t)atoi(hl) : 2u;
   coarse_slots(g, P);
   return P;
 }
@@ -1026,10 +1049,13 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   if (!attr) {
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kDqSmem));
-    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<true>,
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
-    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<false>,
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<false>::Smem));
     attr = true;
@@ -1039,12 +1065,25 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   LLSA_LAUNCH_CHECK("tc_dq_kernel");
   LLSA_MARK(mk, "bwd_dq", s);
   if (P.ncl) {
-    const uint64_t tasks = P.cl_tasks[P.ncl];
-    const uint64_t warps = tasks * units;
-    tc_kv_kernel<true><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
-                         KvCfg<true>::Smem, s>>>(P, tasks, units);
-    count_launch();
-    LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse>");
+    // slots ascend by level: [0, a) hi-only, [a, ncl) hi + lo
+    uint32_t a = 0;
+    while (a < P.ncl && P.cl_level[a] < P.hilo_level) ++a;
+    if (a < P.ncl) {
+      const uint64_t tasks = P.cl_tasks[P.ncl] - P.cl_tasks[a];
+      const uint64_t warps = tasks * units;
+      tc_kv_kernel<2><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
+                        KvCfg<true>::Smem, s>>>(P, tasks, units, a);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse hi+lo>");
+    }
+    if (a > 0) {
+      const uint64_t tasks = P.cl_tasks[a];
+      const uint64_t warps = tasks * units;
+      tc_kv_kernel<1><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
+                        KvCfg<true>::Smem, s>>>(P, tasks, units, 0);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse hi>");
+    }
     reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units);
     count_launch();
     LLSA_LAUNCH_CHECK("reduce_parts_kernel");
@@ -1053,8 +1092,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   {
     const uint64_t tasks = g.n / kBS;
     const uint64_t warps = tasks * units;
-    tc_kv_kernel<false><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
-                          KvCfg<false>::Smem, s>>>(P, tasks, units);
+    tc_kv_kernel<0><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
+                      KvCfg<false>::Smem, s>>>(P, tasks, units, 0);
     count_launch();
     LLSA_LAUNCH_CHECK("tc_kv_kernel<fine>");
   }
