@@ -79,6 +79,11 @@ def build(verbose: bool = False, force: bool = False) -> dict[str, str]:
         _run([CXX] + CXX_FLAGS + ["-shared", "-o", SHIM_LIB] + shim_src +
              [f"-L{OUT}", "-lllsa_cuda", "-Wl,-rpath,$ORIGIN",
               "-L/usr/local/cuda/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
+    # tcgen05 primitive self-test library (tests/test_gpu_umma.py)
+    st_src = sorted(glob.glob(os.path.join(CSRC, "selftest", "*.cu")))
+    st_lib = os.path.join(PKG, "build", "libllsa_umma_selftest.so")
+    if st_src and (force or _stale(st_lib, st_src + hdrs)):
+        _run([NVCC] + NVCC_FLAGS + ["-shared", "-o", st_lib] + st_src)
     # C++ parity tests of the drop-in API (tests/cpp), run by tests/test_cpp_shim.py
     tests_cpp = os.path.join(ROOT, "tests", "cpp")
     built_tests = []

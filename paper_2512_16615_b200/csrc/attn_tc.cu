@@ -34,6 +34,7 @@
 #include "internal.h"
 #include "tc.h"
 #include "tc_common.cuh"
+#include "umma.cuh"
 
 namespace llsa_impl {
 namespace {
@@ -79,6 +80,17 @@ struct TcParams {
   uint64_t cl_part_off[kMaxLevels + 2];  // float offset of slot (per unit)
   float cl_ck[kMaxLevels + 2], cl_cv[kMaxLevels + 2];
   uint64_t part_unit_stride;  // floats per unit (dk + dv)
+  // tcgen05 row-major coarse dK/dV (levels 1..lim-1): one task per
+  // (level, selection row, query slice, 8-block key group)
+  float* rpart;                           // row partials
+  uint32_t rows_on, groups;               // path enabled; key groups per row (K/8)
+  uint32_t rl_count;                      // levels handled (1..lim-1)
+  uint32_t rl_level[kMaxLevels + 2];
+  uint32_t rl_slices[kMaxLevels + 2];     // query slices per row
+  uint64_t rl_qs[kMaxLevels + 2];         // queries per slice
+  uint64_t rl_tasks[kMaxLevels + 3];      // task prefix (per unit)
+  uint64_t rl_part_off[kMaxLevels + 2];   // float offset per unit
+  uint64_t rpart_unit_stride;
 };
 
 // Coarse entry e of the tile whose first fine block is fb0 → (level, first
@@ -856,9 +868,299 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
   }
 }
 
-// split 0 of every coarse slot ← coefficient · Σ_splits (fixed order)
-__global__ void reduce_parts_kernel(TcParams p, uint32_t units) {
-  for (uint32_t sl = 0; sl < p.ncl; ++sl) {
+// ---------------------------------------------------------------------------
+// backward: coarse dK'/dV' on the 5th-gen tensor cores (tcgen05 + TMEM)
+// ---------------------------------------------------------------------------
+// Task = (level l, selection row r, query slice, key group of 8 blocks).  The
+// 128 keys of the group (A operands, K-major, M = 128 = one TMEM lane each)
+// are attended by every query of row r (span B^(l+1)), which streams through
+// a double-buffered 64-query ring (B operands).  Per tile:
+//   S^T  = K' Q^T   and dP^T = V' dO^T   (hi [+ lo]), N = 64 → TMEM
+//   thread = key: P^T = exp2(S^T c + b − lse2_q), dS^T = P^T∘(dP^T − D_q)
+//   → bf16 smem tiles [key][q] (K-major A)
+//   dV' += P^T dO,  dK' += dS^T Q   (B = dO, Q as MN-major [q][d]) → TMEM
+// One elected thread issues every tcgen05.mma; completion is tracked with
+// tcgen05.commit → mbarrier.  The 128×64 dK', dV' partial of the task is
+// written once; rows_reduce_kernel sums them per key block over its CSC
+// segment in ascending row order (deterministic, no atomics).
+namespace rows {
+constexpr int kKeys = 128, kQT = 64;
+constexpr int kKeyTile = kKeys * 128;                // 16 KB
+constexpr int kQTile = kQT * 128;                     // 8 KB
+constexpr int kStage = 2 * kQTile + 2 * kQT * 4;      // Q, dO, lse2, D
+constexpr int kStageAl = (kStage + 1023) & ~1023;     // 17 KB
+constexpr int kOffK = 0;                              // Khi, Klo, Vhi, Vlo
+constexpr int kOffStage = 4 * kKeyTile;               // 64 KB
+constexpr int kOffPT = kOffStage + 2 * kStageAl;      // P^T  [key][q]
+constexpr int kOffDST = kOffPT + kKeys * kQT * 2;     // dS^T [key][q]
+constexpr int kOffBar = kOffDST + kKeys * kQT * 2;
+constexpr int kSmem = kOffBar + 64 + 1024;            // + alignment slack
+constexpr uint32_t kTmemCols = 256;                   // S^T | dP^T | dK' | dV'
+}  // namespace rows
+
+template <bool LO>
+__global__ void __launch_bounds__(256, 1)
+    tc5_kv_rows_kernel(TcParams p, uint32_t li, uint32_t units) {
+  using namespace llsa_umma;
+  using namespace rows;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t tasks_per_unit = p.rl_tasks[li + 1] - p.rl_tasks[li];
+  const uint64_t task_g = blockIdx.x;
+  const uint32_t unit = (uint32_t)(task_g / tasks_per_unit);
+  if (unit >= units) return;
+  uint64_t task = task_g % tasks_per_unit;
+  const uint32_t level = p.rl_level[li];
+  const uint32_t slices = p.rl_slices[li];
+  const uint32_t group = (uint32_t)(task % p.groups);
+  const uint64_t rs = task / p.groups;
+  const uint32_t slice = (uint32_t)(rs % slices);
+  const uint64_t row = rs / slices;
+  const uint64_t span = p.pow[level + 1];
+  const uint64_t q_begin = row * span + (uint64_t)slice * p.rl_qs[li];
+  const uint32_t ntiles = (uint32_t)(p.rl_qs[li] / kQT);
+
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sKhi = sbase + kOffK, sKlo = sKhi + kKeyTile, sVhi = sKlo + kKeyTile,
+                 sVlo = sVhi + kKeyTile;
+  const uint32_t sPT = sbase + kOffPT, sDST = sbase + kOffDST;
+  const uint32_t mbar_s = sbase + kOffBar, mbar_kv = mbar_s + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
+
+  const uint64_t in_off = (uint64_t)unit * p.n * kD;
+  const uint64_t pyr_off = (uint64_t)unit * p.pyr_rows * kD;
+  const uint64_t ro = (uint64_t)unit * p.n;
+  const uint32_t* trow = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level] +
+                         row * p.K + group * 8;
+  const uint64_t nblk = p.n / p.pow[level + 1];
+
+  // key group: 8 selected blocks × 16 rows of K', V' (hi [, lo])
+  for (uint32_t i = tid; i < 8 * 16 * 8; i += blockDim.x) {
+    const uint32_t key = i >> 3, ch = i & 7;
+    uint32_t b = trow[key >> 4];
+    if (b >= nblk) b = 0;
+    const uint64_t grow = p.pyr_off[level] + (uint64_t)b * kBS + (key & 15);
+    const uint64_t src = pyr_off + grow * kD + ch * 8;
+    cp_async16(sKhi + swz(key, ch), p.khi + src);
+    cp_async16(sVhi + swz(key, ch), p.vhi + src);
+    if (LO) {
+      cp_async16(sKlo + swz(key, ch), p.klo + src);
+      cp_async16(sVlo + swz(key, ch), p.vlo + src);
+    }
+  }
+  auto load_tile = [&](uint32_t j, uint32_t stage) {
+    const uint64_t t0 = q_begin + (uint64_t)j * kQT;
+    const uint32_t base = sbase + kOffStage + stage * kStageAl;
+    load_rows_async(base, 0, p.q + in_off + t0 * kD, kQT, tid, blockDim.x);
+    load_rows_async(base + kQTile, 0, p.dout + in_off + t0 * kD, kQT, tid, blockDim.x);
+    if (tid < 16) cp_async16(base + 2 * kQTile + tid * 16, p.lse2 + ro + t0 + tid * 4);
+    else if (tid < 32)
+      cp_async16(base + 2 * kQTile + kQT * 4 + (tid - 16) * 16, p.drow + ro + t0 + (tid - 16) * 4);
+  };
+  load_tile(0, 0);
+  cp_async_commit();
+
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    mbar_init(mbar_s, 1);
+    mbar_init(mbar_kv, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tP = tmem + 64, tDK = tmem + 128, tDV = tmem + 192;
+  const uint32_t idesc_s = idesc_bf16(128, kQT, false, false);  // A, B K-major
+  const uint32_t idesc_kv = idesc_bf16(128, kD, false, true);   // B MN-major
+  const float c = p.scale * kLog2e;
+  const float bias = p.bias2[level];
+  const uint32_t krow = 32 * (warp & 3) + lane;   // this thread's key (TMEM lane)
+  const uint32_t qhalf = warp >> 2;               // query columns [32 qhalf, +32)
+  const uint32_t lane_off = (32u * (warp & 3)) << 16;
+  uint32_t kv_done = 0;
+  auto ensure_kv = [&](uint32_t n) {
+    while (kv_done < n) {
+      mbar_wait(mbar_kv, kv_done & 1);
+      ++kv_done;
+    }
+  };
+
+  for (uint32_t j = 0; j < ntiles; ++j) {
+    const uint32_t st = j & 1;
+    if (j + 1 < ntiles) {
+      ensure_kv(j);  // tile j-1's MMAs read stage (j+1)&1
+      load_tile(j + 1, st ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    fence_proxy_async();
+    __syncthreads();
+    const uint32_t sQ = sbase + kOffStage + st * kStageAl, sG = sQ + kQTile;
+    if (tid == 0) {
+      fence_after();
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t bq = desc_kmajor(sQ + ks * kKStepKMajor);
+        const uint64_t bg = desc_kmajor(sG + ks * kKStepKMajor);
+        mma_bf16(tS, desc_kmajor(sKhi + ks * kKStepKMajor), bq, idesc_s, ks > 0);
+        if (LO) mma_bf16(tS, desc_kmajor(sKlo + ks * kKStepKMajor), bq, idesc_s, 1);
+        mma_bf16(tP, desc_kmajor(sVhi + ks * kKStepKMajor), bg, idesc_s, ks > 0);
+        if (LO) mma_bf16(tP, desc_kmajor(sVlo + ks * kKStepKMajor), bg, idesc_s, 1);
+      }
+      commit(mbar_s);
+    }
+    mbar_wait(mbar_s, j & 1);
+    fence_after();
+    ensure_kv(j);  // P^T / dS^T tiles free (tile j-1's dV/dK done)
+    uint32_t sv[32], pv[32];
+    tmem_ld32(tS + lane_off + qhalf * 32, sv);
+    tmem_ld32(tP + lane_off + qhalf * 32, pv);
+    tmem_ld_wait();
+    const float* lse = reinterpret_cast<const float*>(smem + kOffStage + st * kStageAl + 2 * kQTile);
+    const float* Dq = lse + kQT;
+#pragma unroll
+    for (int c8 = 0; c8 < 4; ++c8) {
+      uint32_t pk[4], dk4[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float pe[2], de[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = c8 * 8 + h * 2 + e;
+          const int q = qhalf * 32 + i;
+          const float pr = ex2(fmaf(__uint_as_float(sv[i]), c, bias) - lse[q]);
+          pe[e] = pr;
+          de[e] = pr * (__uint_as_float(pv[i]) - Dq[q]);
+        }
+        pk[h] = pack_bf16(pe[0], pe[1]);
+        dk4[h] = pack_bf16(de[0], de[1]);
+      }
+      const uint32_t chunk = qhalf * 4 + c8;
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sPT + swz(krow, chunk)),
+                   "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+      asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sDST + swz(krow, chunk)),
+                   "r"(dk4[0]), "r"(dk4[1]), "r"(dk4[2]), "r"(dk4[3]));
+    }
+    fence_proxy_async();
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {  // K = 64 queries
+        mma_bf16(tDV, desc_kmajor(sPT + ks * kKStepKMajor),
+                 desc_mnmajor(sG + ks * kKStepMNMajor, 8192), idesc_kv, (j | ks) > 0);
+        mma_bf16(tDK, desc_kmajor(sDST + ks * kKStepKMajor),
+                 desc_mnmajor(sQ + ks * kKStepMNMajor, 8192), idesc_kv, (j | ks) > 0);
+      }
+      commit(mbar_kv);
+    }
+  }
+  cp_async_wait<0>();
+  ensure_kv(ntiles);
+  fence_after();
+  // raw partial sums of this task: [128 keys][64] dK', then dV'
+  const uint64_t pidx = (row * slices + slice) * p.groups + group;
+  float* dst = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li] +
+               pidx * (2 * kKeys * kD) + (qhalf ? kKeys * kD : 0) + (uint64_t)krow * kD;
+  const uint32_t tsrc = (qhalf ? tDV : tDK) + lane_off;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t r[32];
+    tmem_ld32(tsrc + half * 32, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4*>(dst + half * 32 + i) =
+          make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                      __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
+// Per level-l key block b: Σ over the rows r of its CSC segment (ascending)
+// and over query slices of the partial rows of b's position in row r, scaled
+// by the pooling-adjoint coefficient, into split 0 of the level's slot (the
+// layout tc_kv_kernel<fine> consumes).  One warp per (unit, level, block).
+__global__ void rows_reduce_kernel(TcParams p, uint32_t units, uint64_t warps_per_unit) {
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t unit = (uint32_t)(gw / warps_per_unit);
+  if (unit >= units) return;
+  uint64_t w = gw % warps_per_unit;
+  uint32_t li = 0;
+  uint64_t base_w = 0;
+  for (; li < p.rl_count; ++li) {
+    const uint64_t nb = p.n / p.pow[p.rl_level[li] + 1];
+    if (w < base_w + nb) break;
+    base_w += nb;
+  }
+  if (li >= p.rl_count) return;
+  const uint32_t level = p.rl_level[li];
+  const uint64_t b = w - base_w;
+  const uint32_t slices = p.rl_slices[li];
+  const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[level];
+  const uint32_t* seg =
+      p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[level] + off[b];
+  const uint32_t len = off[b + 1] - off[b];
+  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level];
+  const float* part = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li];
+  // lane: token (lane >> 1) of the block, 32 columns (lane & 1)
+  const uint32_t tok = lane >> 1, c0 = (lane & 1) * 32;
+  float ak[32], av[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) ak[i] = av[i] = 0.f;
+  for (uint32_t si = 0; si < len; ++si) {
+    const uint32_t r = seg[si];
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < p.K; ++j)
+      if (tab[(uint64_t)r * p.K + j] == b) pos = j;
+    const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
+    for (uint32_t s = 0; s < slices; ++s) {
+      const float* src =
+          part + (((uint64_t)r * slices + s) * p.groups + g) * (2 * rows::kKeys * kD);
+      const float4* k4 = reinterpret_cast<const float4*>(src + (uint64_t)key * kD + c0);
+      const float4* v4 =
+          reinterpret_cast<const float4*>(src + rows::kKeys * kD + (uint64_t)key * kD + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 x = k4[i], y = v4[i];
+        ak[4 * i] += x.x;
+        ak[4 * i + 1] += x.y;
+        ak[4 * i + 2] += x.z;
+        ak[4 * i + 3] += x.w;
+        av[4 * i] += y.x;
+        av[4 * i + 1] += y.y;
+        av[4 * i + 2] += y.z;
+        av[4 * i + 3] += y.w;
+      }
+    }
+  }
+  // slot of this level in the coarse-slot table (levels 1..lim-1 come first)
+  uint32_t sl = 0;
+  while (sl < p.ncl && p.cl_level[sl] != level) ++sl;
+  const uint64_t tok_l = p.n / p.pow[level];
+  float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
+  float* gv = gk + (uint64_t)p.cl_split[sl] * tok_l * kD;
+  const uint64_t t = b * kBS + tok;
+  const float ck = p.cl_ck[sl], cv = p.cl_cv[sl];
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    *reinterpret_cast<float4*>(gk + t * kD + c0 + i) =
+        make_float4(ak[i] * ck, ak[i + 1] * ck, ak[i + 2] * ck, ak[i + 3] * ck);
+    *reinterpret_cast<float4*>(gv + t * kD + c0 + i) =
+        make_float4(av[i] * cv, av[i + 1] * cv, av[i + 2] * cv, av[i + 3] * cv);
+  }
+}
+
+// split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
+__global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
+  for (uint32_t sl = s0; sl < s1; ++sl) {
     const uint64_t tok = p.n / p.pow[p.cl_level[sl]];
     const uint64_t elems = tok * kD;
     const uint32_t ns = p.cl_split[sl];
@@ -888,13 +1190,46 @@ uint32_t coarse_entries(const Geometry& g) {
 }
 
 // Coarse kv slots: levels 1..lim-1, then the coarsest when L_e = L.
+// The tcgen05 row-major coarse dK/dV kernel handles levels 1..lim-1 when the
+// selection width is a multiple of 8 blocks (one 128-key group = M).
+bool rows_path(const Geometry& g) {
+  const char* e = getenv("LLSA_NO_TCGEN05");
+  return !(e && e[0] == '1') && g.enrich_lim() >= 2 && g.K % 8 == 0;
+}
+
+void rows_layout(const Geometry& g, TcParams& P) {
+  P.rows_on = rows_path(g) ? 1u : 0u;
+  P.rl_count = 0;
+  P.groups = g.K / 8;
+  uint64_t tasks = 0, off = 0;
+  if (P.rows_on) {
+    for (uint32_t l = 1; l < g.enrich_lim(); ++l) {
+      const uint32_t i = P.rl_count++;
+      const uint64_t span = g.pow[l + 1];
+      const uint64_t qs = span < 1024 ? span : 1024;
+      P.rl_level[i] = l;
+      P.rl_qs[i] = qs;
+      P.rl_slices[i] = (uint32_t)(span / qs);
+      P.rl_tasks[i] = tasks;
+      const uint64_t parts = g.level_blocks(l) * P.rl_slices[i] * P.groups;
+      tasks += parts;
+      P.rl_part_off[i] = off;
+      off += parts * 2 * rows::kKeys * kD;
+    }
+  }
+  P.rl_tasks[P.rl_count] = tasks;
+  P.rpart_unit_stride = off;
+}
+
 void coarse_slots(const Geometry& g, TcParams& P) {
   P.ncl = 0;
   uint64_t tasks = 0, off = 0;
+  const bool rows = rows_path(g);
   auto add = [&](uint32_t l, uint64_t avg_queries, uint64_t blocks) {
     const uint32_t i = P.ncl++;
     uint64_t s = avg_queries / 2048;
     s = s < 1 ? 1 : s > 256 ? 256 : s;
+    if (rows && l < g.enrich_lim()) s = 1;  // reduced by rows_reduce_kernel
     P.cl_level[i] = l;
     P.cl_split[i] = (uint32_t)s;
     P.cl_tasks[i] = tasks;
@@ -939,6 +1274,7 @@ TcParams make_params(const Geometry& g) {
   const char* hl = getenv("LLSA_HILO_LEVEL");  // 1: hi + lo on every coarse level
   P.hilo_level = hl ? (uint32_t)atoi(hl) : 2u;
   coarse_slots(g, P);
+  rows_layout(g, P);
   return P;
 }
 
@@ -1010,8 +1346,10 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
 size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units) {
   TcParams P{};
   coarse_slots(g, P);
+  rows_layout(g, P);
   const size_t rows = ((size_t)units * g.n * 4 + 255) & ~size_t(255);
-  return 2 * rows + (size_t)units * P.part_unit_stride * 4 + 256;
+  const size_t part = ((size_t)units * P.part_unit_stride * 4 + 255) & ~size_t(255);
+  return 2 * rows + part + (size_t)units * P.rpart_unit_stride * 4 + 256;
 }
 
 llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
@@ -1042,6 +1380,9 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   P.lse2 = static_cast<float*>(ws);
   P.drow = reinterpret_cast<float*>(static_cast<char*>(ws) + rows);
   P.part = reinterpret_cast<float*>(static_cast<char*>(ws) + 2 * rows);
+  P.rpart = reinterpret_cast<float*>(
+      static_cast<char*>(ws) + 2 * rows +
+      (((size_t)units * P.part_unit_stride * 4 + 255) & ~size_t(255)));
   P.dq = dq;
   P.dk = dk;
   P.dv = dv;
@@ -1055,6 +1396,10 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rows::kSmem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rows::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<false>::Smem));
@@ -1064,9 +1409,28 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   count_launch();
   LLSA_LAUNCH_CHECK("tc_dq_kernel");
   LLSA_MARK(mk, "bwd_dq", s);
-  if (P.ncl) {
-    // slots ascend by level: [0, a) hi-only, [a, ncl) hi + lo
-    uint32_t a = 0;
+  // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
+  const uint32_t start = P.rows_on ? P.rl_count : 0;
+  if (P.rows_on) {
+    for (uint32_t li = 0; li < P.rl_count; ++li) {
+      const uint64_t tasks = (P.rl_tasks[li + 1] - P.rl_tasks[li]) * units;
+      if (P.rl_level[li] >= P.hilo_level)
+        tc5_kv_rows_kernel<true><<<(unsigned)tasks, 256, rows::kSmem, s>>>(P, li, units);
+      else
+        tc5_kv_rows_kernel<false><<<(unsigned)tasks, 256, rows::kSmem, s>>>(P, li, units);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc5_kv_rows_kernel");
+    }
+    uint64_t wpu = 0;
+    for (uint32_t li = 0; li < P.rl_count; ++li) wpu += g.level_blocks(P.rl_level[li]);
+    rows_reduce_kernel<<<(unsigned)((wpu * units * 32 + 255) / 256), 256, 0, s>>>(P, units, wpu);
+    count_launch();
+    LLSA_LAUNCH_CHECK("rows_reduce_kernel");
+  }
+  LLSA_MARK(mk, "bwd_kv_coarse_tc5", s);
+  if (start < P.ncl) {
+    // slots ascend by level: [start, a) hi-only, [a, ncl) hi + lo
+    uint32_t a = start;
     while (a < P.ncl && P.cl_level[a] < P.hilo_level) ++a;
     if (a < P.ncl) {
       const uint64_t tasks = P.cl_tasks[P.ncl] - P.cl_tasks[a];
@@ -1076,15 +1440,16 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       count_launch();
       LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse hi+lo>");
     }
-    if (a > 0) {
-      const uint64_t tasks = P.cl_tasks[a];
+    if (a > start) {
+      const uint64_t tasks = P.cl_tasks[a] - P.cl_tasks[start];
       const uint64_t warps = tasks * units;
       tc_kv_kernel<1><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
-                        KvCfg<true>::Smem, s>>>(P, tasks, units, 0);
+                        KvCfg<true>::Smem, s>>>(P, tasks, units, start);
       count_launch();
       LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse hi>");
     }
-    reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units);
+    reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units, start,
+                                                                            P.ncl);
     count_launch();
     LLSA_LAUNCH_CHECK("reduce_parts_kernel");
   }
