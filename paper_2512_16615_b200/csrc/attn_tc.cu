@@ -889,20 +889,27 @@ constexpr int kKeyTile = kKeys * 128;                // 16 KB
 constexpr int kQTile = kQT * 128;                     // 8 KB
 constexpr int kStage = 2 * kQTile + 2 * kQT * 4;      // Q, dO, lse2, D
 constexpr int kStageAl = (kStage + 1023) & ~1023;     // 17 KB
-constexpr int kOffK = 0;                              // Khi, Klo, Vhi, Vlo
-constexpr int kOffStage = 4 * kKeyTile;               // 64 KB
-constexpr int kOffPT = kOffStage + 2 * kStageAl;      // P^T  [key][q]
-constexpr int kOffDST = kOffPT + kKeys * kQT * 2;     // dS^T [key][q]
-constexpr int kOffBar = kOffDST + kKeys * kQT * 2;
-constexpr int kSmem = kOffBar + 64 + 1024;            // + alignment slack
+// smem: key tiles Khi, Vhi (, Klo, Vlo) | 2 query stages | P^T | dS^T | barriers
+template <bool LO>
+struct Layout {
+  static constexpr int kOffStage = (LO ? 4 : 2) * kKeyTile;
+  static constexpr int kOffPT = kOffStage + 2 * kStageAl;      // P^T  [key][q]
+  static constexpr int kOffDST = kOffPT + kKeys * kQT * 2;     // dS^T [key][q]
+  static constexpr int kOffBar = kOffDST + kKeys * kQT * 2;
+  static constexpr int kSmem = kOffBar + 64 + 1024;            // 131 KB / 99 KB
+  static constexpr int kMinBlocks = LO ? 1 : 2;
+};
 constexpr uint32_t kTmemCols = 256;                   // S^T | dP^T | dK' | dV'
 }  // namespace rows
 
 template <bool LO>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, rows::Layout<LO>::kMinBlocks)
     tc5_kv_rows_kernel(TcParams p, uint32_t li, uint32_t units) {
   using namespace llsa_umma;
   using namespace rows;
+  using L = Layout<LO>;
+  constexpr int kOffStage = L::kOffStage, kOffPT = L::kOffPT, kOffDST = L::kOffDST,
+                kOffBar = L::kOffBar;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -923,8 +930,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t ntiles = (uint32_t)(p.rl_qs[li] / kQT);
 
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sKhi = sbase + kOffK, sKlo = sKhi + kKeyTile, sVhi = sKlo + kKeyTile,
-                 sVlo = sVhi + kKeyTile;
+  const uint32_t sKhi = sbase, sVhi = sKhi + kKeyTile, sKlo = sVhi + kKeyTile,
+                 sVlo = sKlo + kKeyTile;
   const uint32_t sPT = sbase + kOffPT, sDST = sbase + kOffDST;
   const uint32_t mbar_s = sbase + kOffBar, mbar_kv = mbar_s + 8;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
@@ -1086,13 +1093,15 @@ __global__ void __launch_bounds__(256, 1)
 // Per level-l key block b: Σ over the rows r of its CSC segment (ascending)
 // and over query slices of the partial rows of b's position in row r, scaled
 // by the pooling-adjoint coefficient, into split 0 of the level's slot (the
-// layout tc_kv_kernel<fine> consumes).  One warp per (unit, level, block).
-__global__ void rows_reduce_kernel(TcParams p, uint32_t units, uint64_t warps_per_unit) {
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t unit = (uint32_t)(gw / warps_per_unit);
+// layout tc_kv_kernel<fine> consumes).  One CTA per (unit, level, block);
+// thread = (token, 4 columns), so every partial row is read with full
+// 128-bit coalescing and ~2·len·slices independent loads in flight.
+__global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t units,
+                                                          uint64_t blocks_per_unit) {
+  const uint64_t cta = blockIdx.x;
+  const uint32_t unit = (uint32_t)(cta / blocks_per_unit);
   if (unit >= units) return;
-  uint64_t w = gw % warps_per_unit;
+  uint64_t w = cta % blocks_per_unit;
   uint32_t li = 0;
   uint64_t base_w = 0;
   for (; li < p.rl_count; ++li) {
@@ -1110,35 +1119,29 @@ __global__ void rows_reduce_kernel(TcParams p, uint32_t units, uint64_t warps_pe
   const uint32_t len = off[b + 1] - off[b];
   const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level];
   const float* part = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li];
-  // lane: token (lane >> 1) of the block, 32 columns (lane & 1)
-  const uint32_t tok = lane >> 1, c0 = (lane & 1) * 32;
-  float ak[32], av[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) ak[i] = av[i] = 0.f;
+  const uint32_t tok = threadIdx.x >> 4, c4 = (threadIdx.x & 15) * 4;
+  float4 ak = make_float4(0.f, 0.f, 0.f, 0.f), av = ak;
   for (uint32_t si = 0; si < len; ++si) {
     const uint32_t r = seg[si];
     uint32_t pos = 0;
     for (uint32_t j = 0; j < p.K; ++j)
       if (tab[(uint64_t)r * p.K + j] == b) pos = j;
     const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
+    const float* src0 = part + ((uint64_t)r * slices * p.groups + g) * (2 * rows::kKeys * kD) +
+                        (uint64_t)key * kD + c4;
+#pragma unroll 4
     for (uint32_t s = 0; s < slices; ++s) {
-      const float* src =
-          part + (((uint64_t)r * slices + s) * p.groups + g) * (2 * rows::kKeys * kD);
-      const float4* k4 = reinterpret_cast<const float4*>(src + (uint64_t)key * kD + c0);
-      const float4* v4 =
-          reinterpret_cast<const float4*>(src + rows::kKeys * kD + (uint64_t)key * kD + c0);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 x = k4[i], y = v4[i];
-        ak[4 * i] += x.x;
-        ak[4 * i + 1] += x.y;
-        ak[4 * i + 2] += x.z;
-        ak[4 * i + 3] += x.w;
-        av[4 * i] += y.x;
-        av[4 * i + 1] += y.y;
-        av[4 * i + 2] += y.z;
-        av[4 * i + 3] += y.w;
-      }
+      const float* src = src0 + (uint64_t)s * p.groups * (2 * rows::kKeys * kD);
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+      const float4 y = __ldg(reinterpret_cast<const float4*>(src + rows::kKeys * kD));
+      ak.x += x.x;
+      ak.y += x.y;
+      ak.z += x.z;
+      ak.w += x.w;
+      av.x += y.x;
+      av.y += y.y;
+      av.z += y.z;
+      av.w += y.w;
     }
   }
   // slot of this level in the coarse-slot table (levels 1..lim-1 come first)
@@ -1149,13 +1152,8 @@ __global__ void rows_reduce_kernel(TcParams p, uint32_t units, uint64_t warps_pe
   float* gv = gk + (uint64_t)p.cl_split[sl] * tok_l * kD;
   const uint64_t t = b * kBS + tok;
   const float ck = p.cl_ck[sl], cv = p.cl_cv[sl];
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) {
-    *reinterpret_cast<float4*>(gk + t * kD + c0 + i) =
-        make_float4(ak[i] * ck, ak[i + 1] * ck, ak[i + 2] * ck, ak[i + 3] * ck);
-    *reinterpret_cast<float4*>(gv + t * kD + c0 + i) =
-        make_float4(av[i] * cv, av[i + 1] * cv, av[i + 2] * cv, av[i + 3] * cv);
-  }
+  *reinterpret_cast<float4*>(gk + t * kD + c4) = make_float4(ak.x * ck, ak.y * ck, ak.z * ck, ak.w * ck);
+  *reinterpret_cast<float4*>(gv + t * kD + c4) = make_float4(av.x * cv, av.y * cv, av.z * cv, av.w * cv);
 }
 
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
@@ -1397,9 +1395,11 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rows::kSmem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       rows::Layout<true>::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rows::kSmem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       rows::Layout<false>::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<false>::Smem));
@@ -1415,15 +1415,17 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     for (uint32_t li = 0; li < P.rl_count; ++li) {
       const uint64_t tasks = (P.rl_tasks[li + 1] - P.rl_tasks[li]) * units;
       if (P.rl_level[li] >= P.hilo_level)
-        tc5_kv_rows_kernel<true><<<(unsigned)tasks, 256, rows::kSmem, s>>>(P, li, units);
+        tc5_kv_rows_kernel<true><<<(unsigned)tasks, 256, rows::Layout<true>::kSmem, s>>>(
+            P, li, units);
       else
-        tc5_kv_rows_kernel<false><<<(unsigned)tasks, 256, rows::kSmem, s>>>(P, li, units);
+        tc5_kv_rows_kernel<false><<<(unsigned)tasks, 256, rows::Layout<false>::kSmem, s>>>(
+            P, li, units);
       count_launch();
       LLSA_LAUNCH_CHECK("tc5_kv_rows_kernel");
     }
     uint64_t wpu = 0;
     for (uint32_t li = 0; li < P.rl_count; ++li) wpu += g.level_blocks(P.rl_level[li]);
-    rows_reduce_kernel<<<(unsigned)((wpu * units * 32 + 255) / 256), 256, 0, s>>>(P, units, wpu);
+    rows_reduce_kernel<<<(unsigned)(wpu * units), 256, 0, s>>>(P, units, wpu);
     count_launch();
     LLSA_LAUNCH_CHECK("rows_reduce_kernel");
   }
