@@ -1156,6 +1156,190 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   *reinterpret_cast<float4*>(gv + t * kD + c4) = make_float4(av.x * cv, av.y * cv, av.z * cv, av.w * cv);
 }
 
+// ---------------------------------------------------------------------------
+// backward: dq over the coarse keys on tcgen05 (query-major, M = 128 queries)
+// ---------------------------------------------------------------------------
+// The CTA's 128 queries share their coarse set (levels 1..L), streamed in
+// chunks of up to 4 entries (64 keys, double-buffered cp.async):
+//   S = Q K'^T, dP = dO V'^T (hi [+ lo]) → TMEM (N = 16·entries)
+//   thread = query row: dS = P∘(dP − D), P = exp2(S c + b − lse2) → bf16 tile
+//   dQ += dS K'_hi (A = dS K-major, B = K' MN-major) → TMEM, whole tile
+// and finally dq[t] += scale · dQ (the fine part was written by tc_dq_kernel
+// with the coarse set skipped, which also produced D and lse2).
+namespace dqc {
+constexpr int kArr = 64 * 128;                 // one 64-key array tile: 8 KB
+constexpr int kStage = 4 * kArr;               // Khi, Vhi, Klo, Vlo
+constexpr int kOffQ = 0, kOffG = 16384, kOffStage = 32768;
+constexpr int kOffDS = kOffStage + 2 * kStage;  // 96 KB
+constexpr int kOffEnt = kOffDS + 16384;         // ce_row[64], ce_lvl[64]
+constexpr int kOffBar = kOffEnt + 2 * kMaxCoarse * 4;
+constexpr int kSmem = kOffBar + 64;             // 112.6 KB: 2 CTAs / SM
+constexpr uint32_t kTmemCols = 256;             // S | dP | dQ
+}  // namespace dqc
+
+__global__ void __launch_bounds__(256, 2) tc5_dq_coarse_kernel(TcParams p) {
+  using namespace llsa_umma;
+  using namespace dqc;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t unit = blockIdx.y;
+  const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
+  const uint64_t fb0 = q0 / kBS;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sQ = sbase + kOffQ, sG = sbase + kOffG, sDS = sbase + kOffDS;
+  uint32_t* ce_row = reinterpret_cast<uint32_t*>(smem + kOffEnt);
+  uint32_t* ce_lvl = ce_row + kMaxCoarse;
+  const uint32_t mbar_s = sbase + kOffBar, mbar_q = mbar_s + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + 16);
+  const uint64_t in_off = (uint64_t)unit * p.n * kD;
+  const uint64_t pyr_off = (uint64_t)unit * p.pyr_rows * kD;
+  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries;
+  const bf16* arrays[4] = {p.khi, p.vhi, p.klo, p.vlo};
+
+  for (uint32_t e = tid; e < p.nce; e += blockDim.x) {
+    uint32_t l, r;
+    coarse_entry(p, tab, fb0, e, l, r);
+    ce_row[e] = r;
+    ce_lvl[e] = l;
+  }
+  __syncthreads();
+  const uint32_t nchunks = (p.nce + 3) / 4;
+  auto chunk_lo = [&](uint32_t ch) {
+    const uint32_t e0 = ch * 4, ne = min(4u, p.nce - e0);
+    bool lo = false;
+    for (uint32_t e = 0; e < ne; ++e) lo |= ce_lvl[e0 + e] >= p.hilo_level;
+    return lo;
+  };
+  auto load_chunk = [&](uint32_t ch, uint32_t stage) {
+    const uint32_t e0 = ch * 4, ne = min(4u, p.nce - e0);
+    load_coarse_chunk(sbase + kOffStage + stage * kStage, kArr, ce_row, e0, ne, arrays,
+                      chunk_lo(ch) ? 4 : 2, pyr_off, tid, blockDim.x);
+  };
+  load_rows_async(sQ, 0, p.q + in_off + q0 * kD, kTileQ, tid, blockDim.x);
+  load_rows_async(sG, 0, p.dout + in_off + q0 * kD, kTileQ, tid, blockDim.x);
+  load_chunk(0, 0);
+  cp_async_commit();
+
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    mbar_init(mbar_s, 1);
+    mbar_init(mbar_q, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tP = tmem + 64, tQ = tmem + 128;
+  const uint32_t row = 32 * (warp & 3) + lane;  // this thread's query (TMEM lane)
+  const uint32_t chalf = warp >> 2;             // key columns [32 chalf, +32)
+  const uint32_t lane_off = (32u * (warp & 3)) << 16;
+  const uint64_t ro = (uint64_t)unit * p.n + q0 + row;
+  const float lse = p.lse2[ro], Drow = p.drow[ro];
+  const float c = p.scale * kLog2e;
+  uint32_t q_done = 0;
+  auto ensure_q = [&](uint32_t n) {
+    while (q_done < n) {
+      mbar_wait(mbar_q, q_done & 1);
+      ++q_done;
+    }
+  };
+
+  for (uint32_t ch = 0; ch < nchunks; ++ch) {
+    const uint32_t st = ch & 1;
+    if (ch + 1 < nchunks) {
+      ensure_q(ch);  // dQ MMA of chunk ch-1 read stage (ch+1)&1
+      load_chunk(ch + 1, st ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    fence_proxy_async();
+    __syncthreads();
+    const uint32_t e0 = ch * 4, ne = min(4u, p.nce - e0);
+    const uint32_t stage = sbase + kOffStage + st * kStage;
+    const uint32_t sKhi = stage, sVhi = stage + kArr, sKlo = stage + 2 * kArr,
+                   sVlo = stage + 3 * kArr;
+    const bool lo = chunk_lo(ch);
+    if (tid == 0) {
+      fence_after();
+      const uint32_t idesc = idesc_bf16(128, 16 * ne, false, false);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t aq = desc_kmajor(sQ + ks * kKStepKMajor);
+        const uint64_t ag = desc_kmajor(sG + ks * kKStepKMajor);
+        mma_bf16(tS, aq, desc_kmajor(sKhi + ks * kKStepKMajor), idesc, ks > 0);
+        mma_bf16(tP, ag, desc_kmajor(sVhi + ks * kKStepKMajor), idesc, ks > 0);
+        if (lo) {
+          mma_bf16(tS, aq, desc_kmajor(sKlo + ks * kKStepKMajor), idesc, 1);
+          mma_bf16(tP, ag, desc_kmajor(sVlo + ks * kKStepKMajor), idesc, 1);
+        }
+      }
+      commit(mbar_s);
+    }
+    mbar_wait(mbar_s, ch & 1);
+    fence_after();
+    ensure_q(ch);  // previous dQ MMA finished reading the dS tile
+    if (chalf * 32 < 16 * ne) {
+      uint32_t sv[32], pv[32];
+      tmem_ld32(tS + lane_off + chalf * 32, sv);
+      tmem_ld32(tP + lane_off + chalf * 32, pv);
+      tmem_ld_wait();
+      const float b0 = p.bias2[ce_lvl[e0 + 2 * chalf]];
+      const float b1 = 2 * chalf + 1 < ne ? p.bias2[ce_lvl[e0 + 2 * chalf + 1]] : 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t pk[4];
+        const float bias = c8 < 2 ? b0 : b1;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float de[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = c8 * 8 + h * 2 + e;
+            const float pr = ex2(fmaf(__uint_as_float(sv[i]), c, bias) - lse);
+            de[e] = pr * (__uint_as_float(pv[i]) - Drow);
+          }
+          pk[h] = pack_bf16(de[0], de[1]);
+        }
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sDS + swz(row, chalf * 4 + c8)),
+                     "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+      }
+    }
+    fence_proxy_async();
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      const uint32_t idesc_q = idesc_bf16(128, kD, false, true);
+      for (uint32_t ks = 0; ks < ne; ++ks)
+        mma_bf16(tQ, desc_kmajor(sDS + ks * kKStepKMajor),
+                 desc_mnmajor(sKhi + ks * kKStepMNMajor, 8192), idesc_q, (ch | ks) > 0);
+      commit(mbar_q);
+    }
+  }
+  cp_async_wait<0>();
+  ensure_q(nchunks);
+  fence_after();
+  {
+    uint32_t r[32];
+    tmem_ld32(tQ + lane_off + chalf * 32, r);
+    tmem_ld_wait();
+    float* d = p.dq + in_off + (q0 + row) * kD + chalf * 32;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 v = *reinterpret_cast<float4*>(d + i);
+      v.x += __uint_as_float(r[i]) * p.scale;
+      v.y += __uint_as_float(r[i + 1]) * p.scale;
+      v.z += __uint_as_float(r[i + 2]) * p.scale;
+      v.w += __uint_as_float(r[i + 3]) * p.scale;
+      *reinterpret_cast<float4*>(d + i) = v;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -1394,6 +1578,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_coarse_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, dqc::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        rows::Layout<true>::kSmem));
@@ -1405,10 +1591,22 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                                        KvCfg<false>::Smem));
     attr = true;
   }
-  tc_dq_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kDqSmem, s>>>(P);
-  count_launch();
-  LLSA_LAUNCH_CHECK("tc_dq_kernel");
+  // dq: fine part (+ D, lse2) on mma.sync; coarse part on tcgen05 when enabled
+  const bool dq5 = P.nce > 0 && rows_path(g);
+  {
+    TcParams Pf = P;
+    if (dq5) Pf.nce = 0;
+    tc_dq_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kDqSmem, s>>>(Pf);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc_dq_kernel");
+  }
   LLSA_MARK(mk, "bwd_dq", s);
+  if (dq5) {
+    tc5_dq_coarse_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, dqc::kSmem, s>>>(P);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc5_dq_coarse_kernel");
+  }
+  LLSA_MARK(mk, "bwd_dq_coarse_tc5", s);
   // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
   const uint32_t start = P.rows_on ? P.rl_count : 0;
   if (P.rows_on) {
