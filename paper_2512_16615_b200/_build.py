@@ -73,7 +73,7 @@ def build(verbose: bool = False, force: bool = False) -> dict[str, str]:
         for f in [ex.submit(_run, j) for j in jobs]:
             f.result()
     if force or jobs or _stale(CUDA_LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB] + objs + ["-lcuda"])
+        _run([NVCC] + ARCH + ["-shared", "-o", CUDA_LIB] + objs)
     shim_src = sorted(glob.glob(os.path.join(CSRC, "shim", "*.cpp")))
     if shim_src and (force or _stale(SHIM_LIB, shim_src + hdrs + [CUDA_LIB])):
         _run([CXX] + CXX_FLAGS + ["-shared", "-o", SHIM_LIB] + shim_src +

@@ -27,6 +27,8 @@
 //     registers — no atomics.  Coarse levels split long query lists into
 //     fixed slices reduced in a fixed order; the fine kernel then adds the
 //     pooling adjoint of every coarse level and writes dk, dv once.
+#include <cuda.h>
+
 #include <cmath>
 #include <cstdlib>
 
@@ -1340,6 +1342,289 @@ __global__ void __launch_bounds__(256, 2) tc5_dq_coarse_kernel(TcParams p) {
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// backward: coarse dq — persistent, warp-specialised tcgen05 pipeline
+// ---------------------------------------------------------------------------
+// One CTA per SM walks query tiles (128 queries, all units).  Roles:
+//   warp 4 (1 lane)  TMA producer: Q/dO tile → 2-stage ring; the coarse
+//                    entries' K'/V' (16-row boxes, hi [+ lo]) → 3-stage ring
+//   warp 5 (1 lane)  MMA issuer: S, dP of chunk c into TMEM buffer c&1, then
+//                    dQ += dS·K' of chunk c-1 into the tile's TMEM dQ buffer
+//   warps 0-3        thread = query row: dS from S, dP (TMEM) → bf16 smem,
+//                    then the tile epilogue dq[t] += scale·dQ
+// Every hand-off is an mbarrier (TMA complete_tx, tcgen05.commit or 128
+// thread arrivals), so loads, MMAs and the elementwise work of consecutive
+// chunks and tiles overlap.
+struct TmaMaps {
+  CUtensorMap q, g, khi, vhi, klo, vlo;
+};
+
+namespace dqp {
+constexpr int kQStage = 2 * kTileQ * 128;  // Q + dO: 32 KB
+constexpr int kArr = 64 * 128;             // 64 keys × 64 d bf16
+constexpr int kCStage = 4 * kArr;          // Khi, Vhi, Klo, Vlo: 32 KB
+constexpr int kOffQ = 0;
+constexpr int kOffC = 2 * kQStage;         // 64 KB
+constexpr int kOffDS = kOffC + 3 * kCStage;  // 160 KB
+constexpr int kOffBar = kOffDS + 2 * 16384;  // 192 KB
+enum { CFULL = 0, CEMPTY = 3, QFULL = 6, QEMPTY = 8, SREADY = 10, TFREE = 12, DSREADY = 14,
+       DSFREE = 16, DQREADY = 18, DQFREE = 20, NBAR = 22 };
+constexpr int kSmem = kOffBar + NBAR * 8 + 16;
+constexpr uint32_t kTmemCols = 512;  // S/dP x2 (256) + dQ x2 (128)
+}  // namespace dqp
+
+__device__ __forceinline__ uint32_t entry_level(const TcParams& p, uint32_t e) {
+  const uint32_t ksel = p.K * (p.lim - 1);
+  return e < ksel ? 1 + e / p.K : p.L;
+}
+
+__global__ void __launch_bounds__(320, 1)
+    tc5_dq_pipe_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TmaMaps m,
+                       uint32_t units) {
+  using namespace llsa_umma;
+  using namespace dqp;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
+  const uint64_t tpu = p.n / kTileQ;
+  const uint64_t total = tpu * units;
+  const uint32_t nce = p.nce, nch = (nce + 3) / 4;
+  auto chunk_ne = [&](uint32_t ch) { return min(4u, nce - ch * 4); };
+  auto chunk_lo = [&](uint32_t ch) {
+    bool lo = false;
+    for (uint32_t e = ch * 4; e < ch * 4 + chunk_ne(ch); ++e)
+      lo |= entry_level(p, e) >= p.hilo_level;
+    return lo;
+  };
+
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(bar(CFULL + i), 1);
+      mbar_init(bar(CEMPTY + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(QFULL + i), 1);
+      mbar_init(bar(QEMPTY + i), 1);
+      mbar_init(bar(SREADY + i), 1);
+      mbar_init(bar(TFREE + i), 256);
+      mbar_init(bar(DSREADY + i), 256);
+      mbar_init(bar(DSFREE + i), 1);
+      mbar_init(bar(DQREADY + i), 1);
+      mbar_init(bar(DQFREE + i), 256);
+    }
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    // The whole warp resolves the tile's coarse rows in parallel (one table
+    // latency per tile, lanes hold entries lane and lane+32); lane 0 issues
+    // the TMA copies.
+    if (lane == 0) {
+      prefetch_map(&m.q);
+      prefetch_map(&m.g);
+      prefetch_map(&m.khi);
+      prefetch_map(&m.vhi);
+      prefetch_map(&m.klo);
+      prefetch_map(&m.vlo);
+    }
+    uint32_t c = 0, i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries;
+      const uint64_t fb0 = q0 / kBS;
+      uint32_t myrow[2] = {0, 0};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const uint32_t e = lane + 32 * k;
+        if (e < nce) {
+          uint32_t l;
+          coarse_entry(p, tab, fb0, e, l, myrow[k]);
+        }
+      }
+      const uint32_t qs = i & 1;
+      if (lane == 0) {
+        if (i >= 2) mbar_wait(bar(QEMPTY + qs), ((i >> 1) - 1) & 1);
+        const uint32_t qdst = sbase + kOffQ + qs * kQStage;
+        mbar_expect_tx(bar(QFULL + qs), kQStage);
+        tma_load_2d(qdst, &m.q, 0, (int)(unit * p.n + q0), bar(QFULL + qs));
+        tma_load_2d(qdst + kTileQ * 128, &m.g, 0, (int)(unit * p.n + q0), bar(QFULL + qs));
+      }
+      for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+        const uint32_t s = c % 3;
+        const uint32_t ne = chunk_ne(ch);
+        const bool lo = chunk_lo(ch);
+        uint32_t rows4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t ei = ch * 4 + e;
+          const uint32_t v0 = __shfl_sync(0xffffffffu, myrow[0], ei & 31);
+          const uint32_t v1 = __shfl_sync(0xffffffffu, myrow[1], ei & 31);
+          rows4[e] = ei < 32 ? v0 : v1;
+        }
+        if (lane == 0) {
+          if (c >= 3) mbar_wait(bar(CEMPTY + s), ((c / 3) - 1) & 1);
+          const uint32_t dst = sbase + kOffC + s * kCStage;
+          mbar_expect_tx(bar(CFULL + s), ne * (lo ? 4 : 2) * kBS * 128);
+          for (uint32_t e = 0; e < ne; ++e) {
+            const int y = (int)((uint64_t)unit * p.pyr_rows + rows4[e]);
+            tma_load_2d(dst + e * 2048, &m.khi, 0, y, bar(CFULL + s));
+            tma_load_2d(dst + kArr + e * 2048, &m.vhi, 0, y, bar(CFULL + s));
+            if (lo) {
+              tma_load_2d(dst + 2 * kArr + e * 2048, &m.klo, 0, y, bar(CFULL + s));
+              tma_load_2d(dst + 3 * kArr + e * 2048, &m.vlo, 0, y, bar(CFULL + s));
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc_q = idesc_bf16(128, kD, false, true);
+      struct Prev {
+        uint32_t c, s, ne, tp, first, last, ti;
+      } pv{};
+      bool have = false;
+      auto do_dq = [&](const Prev& x) {
+        const uint32_t b = x.c & 1;
+        mbar_wait(bar(DSREADY + b), (x.c >> 1) & 1);
+        if (x.first && x.ti >= 2) mbar_wait(bar(DQFREE + x.tp), ((x.ti >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t sds = sbase + kOffDS + b * 16384;
+        const uint32_t khi = sbase + kOffC + x.s * kCStage;
+        const uint32_t tq = tmem + 256 + x.tp * 64;
+        for (uint32_t ks = 0; ks < x.ne; ++ks)
+          mma_bf16(tq, desc_kmajor(sds + ks * kKStepKMajor),
+                   desc_mnmajor(khi + ks * kKStepMNMajor, 8192), idesc_q,
+                   (x.first && ks == 0) ? 0u : 1u);
+        commit(bar(CEMPTY + x.s));
+        commit(bar(DSFREE + b));
+        if (x.last) commit(bar(DQREADY + x.tp));
+      };
+      uint32_t c = 0, i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t qs = i & 1;
+        mbar_wait(bar(QFULL + qs), (i >> 1) & 1);
+        const uint32_t sq = sbase + kOffQ + qs * kQStage, sg = sq + kTileQ * 128;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+          const uint32_t s = c % 3, b = c & 1;
+          mbar_wait(bar(CFULL + s), (c / 3) & 1);
+          if (c >= 2) mbar_wait(bar(TFREE + b), ((c >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t ne = chunk_ne(ch);
+          const bool lo = chunk_lo(ch);
+          const uint32_t idesc = idesc_bf16(128, 16 * ne, false, false);
+          const uint32_t st = sbase + kOffC + s * kCStage;
+          const uint32_t tS = tmem + b * 128, tP = tS + 64;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t aq = desc_kmajor(sq + ks * kKStepKMajor);
+            const uint64_t ag = desc_kmajor(sg + ks * kKStepKMajor);
+            mma_bf16(tS, aq, desc_kmajor(st + ks * kKStepKMajor), idesc, ks > 0);
+            mma_bf16(tP, ag, desc_kmajor(st + kArr + ks * kKStepKMajor), idesc, ks > 0);
+            if (lo) {
+              mma_bf16(tS, aq, desc_kmajor(st + 2 * kArr + ks * kKStepKMajor), idesc, 1);
+              mma_bf16(tP, ag, desc_kmajor(st + 3 * kArr + ks * kKStepKMajor), idesc, 1);
+            }
+          }
+          commit(bar(SREADY + b));
+          if (ch + 1 == nch) commit(bar(QEMPTY + qs));
+          if (have) do_dq(pv);
+          pv = Prev{c, s, ne, qs, ch == 0 ? 1u : 0u, ch + 1 == nch ? 1u : 0u, i};
+          have = true;
+        }
+      }
+      if (have) do_dq(pv);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    // warp w: TMEM lanes (queries) 32(w&3).., key columns [32(w>>2), +32)
+    const uint32_t row = 32 * (warp & 3) + lane, h = warp >> 2;
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    const float c2 = p.scale * kLog2e;
+    uint32_t c = 0, i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      const uint64_t ro = (uint64_t)unit * p.n + q0 + row;
+      const float lse = p.lse2[ro], Drow = p.drow[ro];
+      float* d = p.dq + ro * kD + h * 32;
+      float4 acc[8];  // this row's dq columns, prefetched for the epilogue
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = reinterpret_cast<const float4*>(d)[k];
+      for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+        const uint32_t b = c & 1;
+        mbar_wait(bar(SREADY + b), (c >> 1) & 1);
+        fence_after();
+        uint32_t sv[32], gv[32];
+        tmem_ld32(tmem + lane_off + b * 128 + h * 32, sv);
+        tmem_ld32(tmem + lane_off + b * 128 + 64 + h * 32, gv);
+        tmem_ld_wait();
+        fence_before();
+        mbar_arrive(bar(TFREE + b));
+        if (c >= 2) mbar_wait(bar(DSFREE + b), ((c >> 1) - 1) & 1);
+        const uint32_t ne = chunk_ne(ch);
+        const uint32_t sds = sbase + kOffDS + b * 16384;
+#pragma unroll
+        for (int ee = 0; ee < 2; ++ee) {
+          const uint32_t e = 2 * h + ee;
+          if (e < ne) {
+            const float bias = p.bias2[entry_level(p, ch * 4 + e)];
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int i0 = ee * 16 + half * 8 + k * 2;
+                const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, bias) - lse);
+                const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, bias) - lse);
+                pk[k] = pack_bf16(p0 * (__uint_as_float(gv[i0]) - Drow),
+                                  p1 * (__uint_as_float(gv[i0 + 1]) - Drow));
+              }
+              asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                               sds + swz(row, e * 2 + half)),
+                           "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+            }
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(bar(DSREADY + b));
+      }
+      // tile epilogue: dq[t] += scale · dQ
+      const uint32_t tp = i & 1;
+      mbar_wait(bar(DQREADY + tp), (i >> 1) & 1);
+      fence_after();
+      uint32_t r0[32];
+      tmem_ld32(tmem + lane_off + 256 + tp * 64 + h * 32, r0);
+      tmem_ld_wait();
+      fence_before();
+      mbar_arrive(bar(DQFREE + tp));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float4 v = acc[k];
+        v.x += __uint_as_float(r0[4 * k]) * p.scale;
+        v.y += __uint_as_float(r0[4 * k + 1]) * p.scale;
+        v.z += __uint_as_float(r0[4 * k + 2]) * p.scale;
+        v.w += __uint_as_float(r0[4 * k + 3]) * p.scale;
+        reinterpret_cast<float4*>(d)[k] = v;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -1480,6 +1765,49 @@ void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out) {
   out->v_lo = reinterpret_cast<bf16*>(base + 3 * a);
 }
 
+// 2-D TMA map over a [rows][64] bf16 tensor, boxes of box_rows × 64,
+// 128-byte swizzle (the K-major / MN-major SW128 operand layout).
+static llsa_status make_tma_map(CUtensorMap* map, const void* base, uint64_t rows,
+                                uint32_t box_rows) {
+  const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kD, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  // resolved through the runtime so the library has no link-time libcuda
+  // dependency (it must load on hosts without a driver)
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !fn)
+      return fail(LLSA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const CUresult r = encode(
+      map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LLSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return LLSA_OK;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* pk,
                                const float* pv, const TcBuffers& tb, cudaStream_t s) {
   float gl[5] = {1, 1, 1, 1, 1};
@@ -1578,6 +1906,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_pipe_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, dqp::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_coarse_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, dqc::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kv_rows_kernel<true>,
@@ -1602,9 +1932,26 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   }
   LLSA_MARK(mk, "bwd_dq", s);
   if (dq5) {
-    tc5_dq_coarse_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, dqc::kSmem, s>>>(P);
-    count_launch();
-    LLSA_LAUNCH_CHECK("tc5_dq_coarse_kernel");
+    const char* old = getenv("LLSA_DQ5_SYNC");
+    if (old && old[0] == '1') {
+      tc5_dq_coarse_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, dqc::kSmem, s>>>(P);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc5_dq_coarse_kernel");
+    } else {
+      TmaMaps maps;
+      const uint64_t in_rows = (uint64_t)units * g.n, pyr_rows = (uint64_t)units * g.pyr_rows;
+      if (llsa_status st = make_tma_map(&maps.q, q, in_rows, kTileQ)) return st;
+      if (llsa_status st = make_tma_map(&maps.g, d_out, in_rows, kTileQ)) return st;
+      if (llsa_status st = make_tma_map(&maps.khi, tb.k_hi, pyr_rows, kBS)) return st;
+      if (llsa_status st = make_tma_map(&maps.vhi, tb.v_hi, pyr_rows, kBS)) return st;
+      if (llsa_status st = make_tma_map(&maps.klo, tb.k_lo, pyr_rows, kBS)) return st;
+      if (llsa_status st = make_tma_map(&maps.vlo, tb.v_lo, pyr_rows, kBS)) return st;
+      const uint64_t tiles = (g.n / kTileQ) * units;
+      const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
+      tc5_dq_pipe_kernel<<<grid, 320, dqp::kSmem, s>>>(P, maps, units);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc5_dq_pipe_kernel");
+    }
   }
   LLSA_MARK(mk, "bwd_dq_coarse_tc5", s);
   // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
