@@ -186,6 +186,63 @@ def reference_sample(steps: int, warmup: int, n: int = N_TOK, L: int = LEVELS,
 
 
 # ---------------------------------------------------------------------------
+# dense comparator (north star: >= 28x faster than dense FlashAttention-style
+# attention at the same shape)
+# ---------------------------------------------------------------------------
+def dense_sdpa(n: int, units: int, dev, steps: int = 3, warmup: int = 2) -> dict:
+    """torch scaled_dot_product_attention (bf16, [1, units, n, 64], non-causal;
+    the fused flash / cuDNN kernel torch picks on this GPU), timed with CUDA
+    events: forward only and forward+backward.  Library kernels, reported
+    beside the LLSA numbers, never as them."""
+    import torch
+    import torch.nn.functional as F
+    shape = (1, units, n, D)
+    q, k, v, g = (torch.randn(shape, device=dev, dtype=torch.bfloat16) for _ in range(4))
+    qr, kr, vr = (t.clone().requires_grad_(True) for t in (q, k, v))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {}
+    with torch.no_grad():
+        for _ in range(warmup):
+            F.scaled_dot_product_attention(q, k, v)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            F.scaled_dot_product_attention(q, k, v)
+        e1.record()
+        torch.cuda.synchronize()
+    res["fwd_ms"] = e0.elapsed_time(e1) / steps
+    for _ in range(warmup):
+        F.scaled_dot_product_attention(qr, kr, vr).backward(g)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        F.scaled_dot_product_attention(qr, kr, vr).backward(g)
+    e1.record()
+    torch.cuda.synchronize()
+    res["fwd_bwd_ms"] = e0.elapsed_time(e1) / steps
+    flops_fwd = 4.0 * n * n * D * units
+    res["fwd_tflops"] = flops_fwd / (res["fwd_ms"] * 1e-3) / 1e12
+    res["fwd_bwd_tflops"] = 3.5 * flops_fwd / (res["fwd_bwd_ms"] * 1e-3) / 1e12
+    res["impl"] = "torch.nn.functional.scaled_dot_product_attention (bf16, non-causal)"
+    del q, k, v, g, qr, kr, vr
+    torch.cuda.empty_cache()
+    return res
+
+
+def _traffic(stage: str):
+    """DRAM bytes per launch of a stage's dominant kernel from the committed ncu
+    capture (profiles/kernel_traffic.json, dram__bytes_read.sum +
+    dram__bytes_write.sum), or None."""
+    p = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        return t.get("stages", {}).get(stage)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,6 +258,8 @@ def main() -> None:
                          "for BASELINE C4 = batch 8 x 16 heads)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true",
+                    help="skip the dense SDPA comparator")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -307,7 +366,7 @@ def main() -> None:
         achieved = wk["bytes"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = _traffic(dom_name)
     roof["kernel"] = dom_name
     roof["kernel_ms"] = dom_ms
     roof["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json, burst)"
@@ -359,6 +418,18 @@ def main() -> None:
             cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {ex}"}
 
+    dense = None
+    if rank == 0 and not args.no_dense:
+        try:
+            dense = dense_sdpa(n, units, dev)
+            fwd_only = sum(t_ for s_, t_ in stages
+                           if s_ in ("compress", "select", "fwd_prep", "fwd_attention"))
+            dense["llsa_fwd_ms"] = fwd_only
+            dense["speedup_fwd"] = dense["fwd_ms"] / fwd_only if fwd_only else None
+            dense["speedup_fwd_bwd"] = dense["fwd_bwd_ms"] / ms
+        except Exception as ex:  # noqa: BLE001
+            dense = {"unavailable": str(ex)[:200]}
+
     if rank == 0:
         line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -371,7 +442,7 @@ def main() -> None:
                 "roofline": roof,
                 "stages_ms": {s: round(t_, 4) for s, t_ in stages},
                 "tensor_cores": h.uses_tensor_cores,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
+                "cpu_baseline": cpu, "e2e": e2e, "dense_sdpa": dense, "gpu_launches": launches * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -74,6 +74,7 @@ struct TcParams {
   // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
   // shallower ones (gain B^l small) use hi only.
   uint32_t hilo_level;
+  uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
   uint32_t cl_level[kMaxLevels + 2];
@@ -94,6 +95,15 @@ struct TcParams {
   uint64_t rl_part_off[kMaxLevels + 2];   // float offset per unit
   uint64_t rpart_unit_stride;
 };
+
+// Pipeline trace (debug only): CTA 0 records (role, tile, event, clock) so the
+// hand-offs of the warp-specialised kernels can be inspected offline.
+__device__ unsigned long long g_trace[8192];  // [role 0..7][tile 0..31][event 0..31]
+__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t role, uint32_t tile,
+                                         uint32_t ev) {
+  if (p.trace && blockIdx.x == 0 && tile < 32 && ev < 32)
+    g_trace[role * 1024 + tile * 32 + ev] = clock64() | (1ull << 63);
+}
 
 // Coarse entry e of the tile whose first fine block is fb0 → (level, first
 // pyramid row), canonical plan order (attention.cpp:107-118).
@@ -1625,6 +1635,450 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// forward — persistent, warp-specialised: coarse keys on tcgen05 / TMEM,
+// fine blocks on mma.sync, running concurrently on separate warps
+// ---------------------------------------------------------------------------
+// One CTA per SM walks 128-query tiles.  The tile's coarse set (levels 1..L,
+// shared by its 8 fine query blocks; <= 24 entries = 384 keys) is a dense
+// M = 128 problem: its whole score block S = Q K'^T lives in TMEM and its
+// softmax is exact (two passes over TMEM: row max, then P), so no TMEM
+// accumulator is ever rescaled.  The fine part (each fine query block's own
+// K gathered level-0 blocks) is block-diagonal and runs on mma.sync.  The
+// two halves are independent softmax partitions merged at the end
+// (m = max(m_f, m_c), O = (O_f 2^(m_f-m) + O_c 2^(m_c-m)) / l).  Roles:
+//   warp 0 (1 lane)  TMA producer: Q tile; coarse K' chunks (hi [+ lo],
+//                    64 keys) → 3-stage ring
+//   warp 2 (1 lane)  TMA producer: coarse V' chunks → 2-stage ring
+//   warp 1 (1 lane)  MMA issuer: S chunks into TMEM; O_c += P·V'_hi chunk by
+//                    chunk as the coarse warps publish P
+//   warps 3-6        coarse softmax, thread = query row (its TMEM lane):
+//                    row max over S, P = exp2(.) → bf16 smem ring (K-major
+//                    A operand of the PV MMA), then O_c (raw) → out, and
+//                    (m_c, l_c) → smem
+//   warps 7-14       fine part, warp 7+w = fine query block w: its K blocks
+//                    streamed by a 3-stage cp.async ring, online softmax in
+//                    registers; then merges with the coarse partial in `out`
+// The producer and MMA warps take the lowest warp ids: the scheduler favours
+// older warps, and starving the single-thread roles stalls the whole tile.
+// Replaces P/src/attention.cpp:166-214 for the tensor-core shapes.
+namespace fw5 {
+constexpr int kQBytes = kTileQ * 128;           // 16 KB
+constexpr int kKRing = 3;                       // K' ring: hi + lo of 64 keys
+constexpr int kKStage = 16384;
+constexpr int kVRing = 2;                       // V' ring: hi of 64 keys
+constexpr int kVStage = 8192;
+constexpr int kPBytes = kTileQ * 128;           // 128 rows x 64 keys bf16
+constexpr int kFineStages = 3;
+constexpr int kQStages = 1;
+constexpr int kFineWarp = kFineStages * 4096;   // per fine warp: {K, V} blocks
+constexpr int kMaxChunks = 6;
+constexpr int kOffQ = 0;
+constexpr int kOffK = kOffQ + kQStages * kQBytes;      // 16 KB
+constexpr int kOffV = kOffK + kKRing * kKStage;        // 64 KB
+constexpr int kOffP = kOffV + kVRing * kVStage;        // 80 KB
+constexpr int kOffFine = kOffP + 2 * kPBytes;          // 112 KB
+constexpr int kOffStat = kOffFine + 8 * kFineWarp;     // 208 KB
+constexpr int kOffEnt = kOffStat + 2 * 2 * kTileQ * 4; // + (m_c, l_c) x 2 tiles
+constexpr int kOffBar = kOffEnt + 512;                 // entry bias[32], chunk info[8], rows[2][32]
+enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 8, VFULL = 12, VEMPTY = 15, SREADY = 18,
+       SFREE = 24, PFULL = 30, PEMPTY = 32, OREADY = 34, OFREE = 36, CDONE = 38, CFREE = 40,
+       NBAR = 42 };
+constexpr int kSmem = kOffBar + NBAR * 8 + 16;
+constexpr int kThreads = 15 * 32;  // 0 K'+Q TMA, 1 MMA, 2 V' TMA, 3-6 coarse, 7-14 fine
+constexpr uint32_t kTmemCols = 512;  // S: [0, 384), O: 384 + 64·buffer
+constexpr uint32_t kMaxEntries = 4 * kMaxChunks;
+}  // namespace fw5
+
+__global__ void __launch_bounds__(fw5::kThreads, 1)
+    tc5_fwd_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TmaMaps m,
+                   uint32_t units) {
+  using namespace llsa_umma;
+  using namespace fw5;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
+  float* cstat = reinterpret_cast<float*>(smem + kOffStat);  // [2][m | l][128]
+  const uint64_t tpu = p.n / kTileQ;
+  const uint64_t total = tpu * units;
+  const uint32_t nce = p.nce, nch = (nce + 3) / 4;
+  auto chunk_ne = [&](uint32_t ch) { return min(4u, nce - ch * 4); };
+  auto chunk_lo = [&](uint32_t ch) {
+    bool lo = false;
+    for (uint32_t e = ch * 4; e < ch * 4 + chunk_ne(ch); ++e)
+      lo |= entry_level(p, e) >= p.hilo_level;
+    return lo;
+  };
+
+  // tile-invariant entry facts, computed once: bias (log2 units) per coarse
+  // entry, and per 64-key chunk its entry count and whether it needs K'_lo
+  float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
+  uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
+  uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 256);  // [K | V][32]
+  if (tid < nce) ent_bias[tid] = p.bias2[entry_level(p, tid)];
+  if (tid < nch) ch_info[tid] = chunk_ne(tid) | (chunk_lo(tid) ? 0x100u : 0u);
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(QFULL + i), 1);
+      mbar_init(bar(QEMPTY + i), 1 + 256);  // S MMAs done + fine warps hold Q
+      mbar_init(bar(PFULL + i), 128);
+      mbar_init(bar(PEMPTY + i), 1);
+      mbar_init(bar(OREADY + i), 1);
+      mbar_init(bar(OFREE + i), 128);
+      mbar_init(bar(CDONE + i), 128);
+      mbar_init(bar(CFREE + i), 256);
+    }
+    for (int i = 0; i < kKRing; ++i) {
+      mbar_init(bar(KFULL + i), 1);
+      mbar_init(bar(KEMPTY + i), 1);
+    }
+    for (int i = 0; i < kVRing; ++i) {
+      mbar_init(bar(VFULL + i), 1);
+      mbar_init(bar(VEMPTY + i), 1);
+    }
+    for (int i = 0; i < kMaxChunks; ++i) {
+      mbar_init(bar(SREADY + i), 1);
+      mbar_init(bar(SFREE + i), 128);
+    }
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0 || warp == 2) {
+    // ------------------------------------------------------------ producers
+    // warp 0: Q tile + coarse K' chunks; warp 2: coarse V' chunks.  Each
+    // resolves the tile's coarse rows itself, so the K' side runs ahead of
+    // the PV side by as many tiles as its ring allows.
+    const bool kside = warp == 0;
+    if (lane == 0) {
+      prefetch_map(kside ? &m.q : &m.vhi);
+      if (kside) {
+        prefetch_map(&m.khi);
+        prefetch_map(&m.klo);
+      }
+    }
+    // The coarse rows are gathered with cp.async by all 32 lanes (16 B per
+    // lane per instruction; a 2 KB entry is 4 per lane) into the 128-byte
+    // swizzled layout the UMMA descriptors expect; a chunk is published
+    // (proxy fence + FULL arrive) once the lanes' copies of it have landed,
+    // one chunk behind the issue front.  Per-entry TMA boxes were issue-bound
+    // here (~150 cycles per 2 KB box).
+    const uint32_t ring = kside ? kKRing : kVRing;
+    uint32_t* rows = ent_rows + (kside ? 0 : 32);
+    const bf16* arr0 = kside ? p.khi : p.vhi;
+    const bf16* arr1 = p.klo;
+    uint32_t rc = 0, i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      if (lane < nce) {
+        uint32_t l, r;
+        coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, q0 / kBS, lane, l, r);
+        rows[lane] = (uint32_t)(unit * p.pyr_rows) + r;
+      }
+      __syncwarp();
+      if (lane == 0) trace_ev(p, kside ? 1 : 2, i, 0);
+      if (kside && lane == 0) {
+        const uint32_t qs = i % kQStages;
+        if (i >= (uint32_t)kQStages) mbar_wait(bar(QEMPTY + qs), ((i / kQStages) - 1) & 1);
+        mbar_expect_tx(bar(QFULL + qs), kQBytes);
+        tma_load_2d(sbase + kOffQ + qs * kQBytes, &m.q, 0, (int)(unit * p.n + q0),
+                    bar(QFULL + qs));
+      }
+      uint32_t prev_full = 0;
+      for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
+        const uint32_t s = rc % ring;
+        const uint32_t info = ch_info[ch], ne = info & 0xFF;
+        const bool lo = kside && (info & 0x100u);
+        if (rc >= ring) mbar_wait(bar((kside ? KEMPTY : VEMPTY) + s), ((rc / ring) - 1) & 1);
+        const uint32_t dst = sbase + (kside ? kOffK + s * kKStage : kOffV + s * kVStage);
+        for (uint32_t e = 0; e < ne; ++e) {
+          const uint64_t row = rows[ch * 4 + e];
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const uint32_t seg = lane + 32 * k4, r = seg >> 3, c = seg & 7;
+            cp_async16(dst + swz(e * 16 + r, c), arr0 + (row + r) * kD + c * 8);
+            if (lo) cp_async16(dst + 8192 + swz(e * 16 + r, c), arr1 + (row + r) * kD + c * 8);
+          }
+        }
+        cp_async_commit();
+        if (prev_full) {
+          cp_async_wait<1>();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(prev_full);
+        }
+        prev_full = bar((kside ? KFULL : VFULL) + s);
+        if (lane == 0) trace_ev(p, kside ? 1 : 2, i, 1 + ch);
+      }
+      cp_async_wait<0>();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0 && prev_full) mbar_arrive(prev_full);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // S chunk c of tile i reuses TMEM columns [64c, 64c+64) as soon as the
+    // coarse warps have read chunk c of tile i-1 (per-chunk SREADY / SFREE).
+    if (lane == 0) {
+      const uint32_t idesc_o = idesc_bf16(128, kD, false, true);
+      uint32_t kc = 0, vc = 0, pc = 0, i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t qs = i % kQStages, ob = i & 1;
+        mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
+        const uint32_t sq = sbase + kOffQ + qs * kQBytes;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
+          const uint32_t s = kc % kKRing;
+          mbar_wait(bar(KFULL + s), (kc / kKRing) & 1);
+          if (i >= 1) mbar_wait(bar(SFREE + ch), (i - 1) & 1);
+          fence_after();
+          const uint32_t ne = ch_info[ch] & 0xFF;
+          const bool lo = ch_info[ch] & 0x100u;
+          const uint32_t idesc = idesc_bf16(128, 16 * ne, false, false);
+          const uint32_t st = sbase + kOffK + s * kKStage;
+          const uint32_t tS = tmem + 64 * ch;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t aq = desc_kmajor(sq + ks * kKStepKMajor);
+            mma_bf16(tS, aq, desc_kmajor(st + ks * kKStepKMajor), idesc, ks > 0);
+            if (lo) mma_bf16(tS, aq, desc_kmajor(st + 8192 + ks * kKStepKMajor), idesc, 1);
+          }
+          commit(bar(KEMPTY + s));
+          commit(bar(SREADY + ch));
+          trace_ev(p, 3, i, ch);
+        }
+        commit(bar(QEMPTY + qs));
+        if (i >= 2) mbar_wait(bar(OFREE + ob), ((i >> 1) - 1) & 1);
+        const uint32_t tO = tmem + 384 + 64 * ob;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++vc, ++pc) {
+          const uint32_t s = vc % kVRing, ps = pc & 1;
+          mbar_wait(bar(VFULL + s), (vc / kVRing) & 1);
+          mbar_wait(bar(PFULL + ps), (pc >> 1) & 1);
+          fence_after();
+          const uint32_t ne = chunk_ne(ch);
+          const uint32_t sp = sbase + kOffP + ps * kPBytes;
+          const uint32_t sv = sbase + kOffV + s * kVStage;
+          for (uint32_t ks = 0; ks < ne; ++ks)
+            mma_bf16(tO, desc_kmajor(sp + ks * kKStepKMajor),
+                     desc_mnmajor(sv + ks * kKStepMNMajor, 8192), idesc_o, (ch | ks) > 0);
+          commit(bar(VEMPTY + s));
+          commit(bar(PEMPTY + ps));
+          trace_ev(p, 3, i, 16 + ch);
+        }
+        commit(bar(OREADY + ob));
+      }
+    }
+  } else if (warp >= 3 && warp < 7) {
+    // ------------------------------------------------------------ coarse warps
+    const uint32_t row = 32 * (warp & 3) + lane;
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    const float c2 = p.scale * kLog2e;
+    uint32_t pc = 0, i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      // pass 1: row max of s·c + b over the coarse set
+      float mx = -INFINITY;
+      for (uint32_t ch = 0; ch < nch; ++ch) {
+        const uint32_t ne = chunk_ne(ch);
+        mbar_wait(bar(SREADY + ch), i & 1);
+        fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (2 * hh < (int)ne) {
+            uint32_t sv[32];
+            tmem_ld32(tmem + lane_off + 64 * ch + 32 * hh, sv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int ee = 0; ee < 2; ++ee) {
+              const uint32_t e = 2 * hh + ee;
+              if (e < ne) {
+                const float bias = ent_bias[ch * 4 + e];
+                float x = __uint_as_float(sv[ee * 16]);
+#pragma unroll
+                for (int k = 1; k < 16; ++k) x = fmaxf(x, __uint_as_float(sv[ee * 16 + k]));
+                mx = fmaxf(mx, fmaf(x, c2, bias));  // c > 0: max(s)·c + b = max(s·c + b)
+              }
+            }
+          }
+        }
+      }
+      if (tid == 96) trace_ev(p, 4, i, 0);
+      // pass 2: P = exp2(s·c + b − m_c) → bf16 ring; l_c
+      float lsum = 0.f;
+      for (uint32_t ch = 0; ch < nch; ++ch, ++pc) {
+        const uint32_t ne = chunk_ne(ch), ps = pc & 1;
+        if (pc >= 2) mbar_wait(bar(PEMPTY + ps), ((pc >> 1) - 1) & 1);
+        const uint32_t sp = sbase + kOffP + ps * kPBytes;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (2 * hh < (int)ne) {
+            uint32_t sv[32];
+            tmem_ld32(tmem + lane_off + 64 * ch + 32 * hh, sv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int ee = 0; ee < 2; ++ee) {
+              const uint32_t e = 2 * hh + ee;
+              if (e < ne) {
+                const float nb = ent_bias[ch * 4 + e] - mx;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                  uint32_t pk[4];
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    const int i0 = ee * 16 + half * 8 + k * 2;
+                    const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
+                    const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
+                    lsum += p0 + p1;
+                    pk[k] = pack_bf16(p0, p1);
+                  }
+                  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                                   sp + swz(row, e * 2 + half)),
+                               "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+                }
+              }
+            }
+          }
+        }
+        fence_before();
+        mbar_arrive(bar(SFREE + ch));
+        fence_proxy_async();
+        mbar_arrive(bar(PFULL + ps));
+      }
+      // O_c (raw) → out; (m_c, l_c) → smem for the fine warps' merge
+      const uint32_t ob = i & 1;
+      if (tid == 96) trace_ev(p, 4, i, 1);
+      mbar_wait(bar(OREADY + ob), (i >> 1) & 1);
+      if (tid == 96) trace_ev(p, 4, i, 2);
+      fence_after();
+      float* o = p.out + (uint64_t)unit * p.n * kD + (q0 + row) * kD;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t ov[32];
+        tmem_ld32(tmem + lane_off + 384 + 64 * ob + 32 * hh, ov);
+        tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          reinterpret_cast<float4*>(o + 32 * hh)[k] =
+              make_float4(__uint_as_float(ov[4 * k]), __uint_as_float(ov[4 * k + 1]),
+                          __uint_as_float(ov[4 * k + 2]), __uint_as_float(ov[4 * k + 3]));
+      }
+      fence_before();
+      mbar_arrive(bar(OFREE + ob));
+      if (i >= 2) mbar_wait(bar(CFREE + ob), ((i >> 1) - 1) & 1);
+      cstat[ob * 256 + row] = mx;
+      cstat[ob * 256 + 128 + row] = lsum;
+      __threadfence_block();
+      mbar_arrive(bar(CDONE + ob));
+      if (tid == 96) trace_ev(p, 4, i, 3);
+    }
+  } else {
+    // ------------------------------------------------------------ fine warps
+    const float c2 = p.scale * kLog2e;
+    const uint32_t fw = warp - 7;  // fine query block of the tile
+    const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
+    const uint64_t nfb = p.n / kBS;
+    const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
+    uint32_t i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      const uint32_t qs = i % kQStages;
+      const uint64_t in_off = (uint64_t)unit * p.n * kD;
+      const uint32_t* frow =
+          p.tables + (uint64_t)unit * p.table_entries + p.table_off[0] + (q0 / kBS + fw) * p.K;
+      auto load_fine = [&](uint32_t j) {
+        uint32_t b = frow[j];
+        if (b >= nfb) {
+          raise_flag(p.flag, llsa_dev::kErrIndex);
+          b = 0;
+        }
+        const uint32_t base = sF + (j % kFineStages) * 4096;
+        load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+        load_rows_async(base + kTile16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+      };
+#pragma unroll
+      for (uint32_t j = 0; j + 1 < (uint32_t)kFineStages; ++j) {
+        if (j < p.K) load_fine(j);
+        cp_async_commit();
+      }
+      SoftmaxState st;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) st.o[j][e] = 0.f;
+      st.m[0] = st.m[1] = -INFINITY;
+      st.l[0] = st.l[1] = 0.f;
+      uint32_t qf[4][4];
+      if (tid == 224) trace_ev(p, 5, i, 0);
+      mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
+      if (tid == 224) trace_ev(p, 5, i, 3);
+      const uint32_t sq = sbase + kOffQ + qs * kQBytes;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) lda(sq, fw * 16, ks, lane, qf[ks]);
+      mbar_arrive(bar(QEMPTY + qs));
+      const float bf = p.bias2[0];
+      for (uint32_t j = 0; j < p.K; ++j) {
+        if (j + kFineStages - 1 < p.K) load_fine(j + kFineStages - 1);
+        cp_async_commit();
+        cp_async_wait<kFineStages - 1>();
+        __syncwarp();
+        const uint32_t base = sF + (j % kFineStages) * 4096;
+        attend_fwd<false>(base, base, base + kTile16, 0, 1, bf, bf, c2, qf, lane, st);
+        __syncwarp();
+      }
+      // merge with the coarse partition of the same rows
+      const uint32_t ob = i & 1;
+      if (tid == 224) trace_ev(p, 5, i, 1);
+      mbar_wait(bar(CDONE + ob), (i >> 1) & 1);
+      if (tid == 224) trace_ev(p, 5, i, 2);
+      const float lf0 = quad_sum(st.l[0]), lf1 = quad_sum(st.l[1]);
+      const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
+      const float mc0 = cstat[ob * 256 + r0], mc1 = cstat[ob * 256 + r1];
+      const float lc0 = cstat[ob * 256 + 128 + r0], lc1 = cstat[ob * 256 + 128 + r1];
+      __syncwarp();
+      mbar_arrive(bar(CFREE + ob));
+      const float m0 = fmaxf(st.m[0], mc0), m1 = fmaxf(st.m[1], mc1);
+      const float af0 = ex2(st.m[0] - m0), ac0 = ex2(mc0 - m0);
+      const float af1 = ex2(st.m[1] - m1), ac1 = ex2(mc1 - m1);
+      const float l0 = lf0 * af0 + lc0 * ac0, l1 = lf1 * af1 + lc1 * ac1;
+      const float i0 = 1.f / l0, i1 = 1.f / l1;
+      float* o0 = p.out + in_off + (q0 + r0) * kD;
+      float* o1 = p.out + in_off + (q0 + r1) * kD;
+      bool bad = !(l0 > 0.f) || !(l1 > 0.f) || !isfinite(l0) || !isfinite(l1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 c0 = __ldcg(reinterpret_cast<const float2*>(o0 + j * 8 + cc));
+        const float2 c1 = __ldcg(reinterpret_cast<const float2*>(o1 + j * 8 + cc));
+        const float2 v0 = make_float2((st.o[j][0] * af0 + c0.x * ac0) * i0,
+                                      (st.o[j][1] * af0 + c0.y * ac0) * i0);
+        const float2 v1 = make_float2((st.o[j][2] * af1 + c1.x * ac1) * i1,
+                                      (st.o[j][3] * af1 + c1.y * ac1) * i1);
+        bad |= !isfinite(v0.x) || !isfinite(v0.y) || !isfinite(v1.x) || !isfinite(v1.y);
+        *reinterpret_cast<float2*>(o0 + j * 8 + cc) = v0;
+        *reinterpret_cast<float2*>(o1 + j * 8 + cc) = v1;
+      }
+      if ((lane & 3) == 0) {
+        const uint64_t ro = (uint64_t)unit * p.n + q0;
+        p.row_max[ro + r0] = m0 / kLog2e;
+        p.row_max[ro + r1] = m1 / kLog2e;
+        p.row_denom[ro + r0] = l0;
+        p.row_denom[ro + r1] = l1;
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) raise_flag(p.flag, llsa_dev::kErrNonFinite);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -1662,6 +2116,14 @@ uint32_t coarse_entries(const Geometry& g) {
 bool rows_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   return !(e && e[0] == '1') && g.enrich_lim() >= 2 && g.K % 8 == 0;
+}
+
+// tcgen05 forward: every coarse entry's scores fit the TMEM S block
+bool fwd5_path(const Geometry& g) {
+  const char* e = getenv("LLSA_NO_TCGEN05");
+  const char* f = getenv("LLSA_FWD5");
+  const uint32_t nce = coarse_entries(g);
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries;
 }
 
 void rows_layout(const Geometry& g, TcParams& P) {
@@ -1738,6 +2200,8 @@ TcParams make_params(const Geometry& g) {
     P.csc_flat_off[l] = g.csc_flat_off[l];
   }
   P.flag = device_flag();
+  const char* tr = getenv("LLSA_TRACE");
+  P.trace = tr && tr[0] == '1' ? 1u : 0u;
   const char* hl = getenv("LLSA_HILO_LEVEL");  // 1: hi + lo on every coarse level
   P.hilo_level = hl ? (uint32_t)atoi(hl) : 2u;
   coarse_slots(g, P);
@@ -1844,11 +2308,27 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
   if (!attr) {
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFwdSmem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_fwd_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, fw5::kSmem));
     attr = true;
   }
-  tc_fwd_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kFwdSmem, s>>>(P);
-  count_launch();
-  LLSA_LAUNCH_CHECK("tc_fwd_kernel");
+  if (fwd5_path(g)) {
+    TmaMaps maps{};
+    const uint64_t in_rows = (uint64_t)units * g.n, pyr_rows = (uint64_t)units * g.pyr_rows;
+    if (llsa_status st = make_tma_map(&maps.q, q, in_rows, kTileQ)) return st;
+    if (llsa_status st = make_tma_map(&maps.khi, tb.k_hi, pyr_rows, kBS)) return st;
+    if (llsa_status st = make_tma_map(&maps.klo, tb.k_lo, pyr_rows, kBS)) return st;
+    if (llsa_status st = make_tma_map(&maps.vhi, tb.v_hi, pyr_rows, kBS)) return st;
+    const uint64_t tiles = (g.n / kTileQ) * units;
+    const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
+    tc5_fwd_kernel<<<grid, fw5::kThreads, fw5::kSmem, s>>>(P, maps, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc5_fwd_kernel");
+  } else {
+    tc_fwd_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kFwdSmem, s>>>(P);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc_fwd_kernel");
+  }
   LLSA_MARK(mk, "fwd_attention", s);
   return LLSA_OK;
 }
@@ -2014,3 +2494,13 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
 }
 
 }  // namespace llsa_impl
+
+// Debug: copies the pipeline trace recorded by CTA 0 (LLSA_TRACE=1) and resets it.
+extern "C" int llsa_debug_trace(unsigned long long* out, int cap) {
+  cudaDeviceSynchronize();
+  const int n = cap < 8192 ? cap : 8192;
+  cudaMemcpyFromSymbol(out, llsa_impl::g_trace, n * sizeof(unsigned long long));
+  static unsigned long long zero[8192];
+  cudaMemcpyToSymbol(llsa_impl::g_trace, zero, sizeof(zero));
+  return n;
+}

@@ -10,8 +10,11 @@
 #include <bit>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <ostream>
 #include <string>
+#include <vector>
 
 #include "llsa/attention.hpp"
 #include "llsa/attention_grad.hpp"
@@ -60,15 +63,75 @@ void ckc(cudaError_t e, const char* what) {
 // NonFiniteError), as the reference does when its loops finish.
 void finish() { ck(llsa_sync_status(nullptr)); }
 
+// Device scratch for the host-buffer API: a process-wide caching pool keyed
+// by power-of-two size class, so a call sequence reuses device memory instead
+// of paying cudaMalloc/cudaFree (an implicit device synchronisation) per
+// call.  Cached blocks are kept up to kPoolCap bytes; beyond that they are
+// returned to the driver.
+class DevicePool {
+ public:
+  static DevicePool& get() {
+    static DevicePool* pool = new DevicePool();  // intentionally leaked: no teardown-order hazards
+    return *pool;
+  }
+  void* acquire(std::size_t bytes, std::size_t* cls_out) {
+    const std::size_t cls = std::bit_ceil(std::max<std::size_t>(bytes, 256));
+    *cls_out = cls;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto it = free_.find(cls);
+      if (it != free_.end() && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        cached_ -= cls;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, cls);
+    if (e != cudaSuccess) {  // release the cache once and retry
+      trim();
+      (void)cudaGetLastError();
+      e = cudaMalloc(&p, cls);
+    }
+    ckc(e, "cudaMalloc");
+    return p;
+  }
+  void release(void* p, std::size_t cls) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (cached_ + cls <= kPoolCap) {
+        free_[cls].push_back(p);
+        cached_ += cls;
+        return;
+      }
+    }
+    cudaFree(p);
+  }
+  void trim() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto& [cls, v] : free_)
+      for (void* p : v) cudaFree(p);
+    free_.clear();
+    cached_ = 0;
+  }
+
+ private:
+  static constexpr std::size_t kPoolCap = std::size_t(4) << 30;
+  std::mutex mu_;
+  std::map<std::size_t, std::vector<void*>> free_;
+  std::size_t cached_ = 0;
+};
+
 template <typename T>
 class DevBuf {
  public:
   explicit DevBuf(std::size_t n) : n_(n) {
-    if (n_) ckc(cudaMalloc(&p_, n_ * sizeof(T)), "cudaMalloc");
+    if (n_) p_ = static_cast<T*>(DevicePool::get().acquire(n_ * sizeof(T), &cls_));
   }
   DevBuf(const T* host, std::size_t n) : DevBuf(n) { upload(host); }
   ~DevBuf() {
-    if (p_) cudaFree(p_);
+    if (p_) DevicePool::get().release(p_, cls_);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -82,7 +145,7 @@ class DevBuf {
 
  private:
   T* p_ = nullptr;
-  std::size_t n_ = 0;
+  std::size_t n_ = 0, cls_ = 0;
 };
 
 llsa_config to_c(const LLSAConfig& c) {

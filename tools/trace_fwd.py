@@ -1,0 +1,33 @@
+"""Debug: runs one forward with LLSA_TRACE=1 and prints CTA 0's pipeline
+timeline (role, tile, event, cycle offset)."""
+import ctypes as C
+import os
+import sys
+
+os.environ["LLSA_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2512_16615_b200 as llsa  # noqa: E402
+
+units, n = 16, 65536
+q, k, v = (torch.randn(units, n, 64, device="cuda").to(torch.bfloat16) for _ in range(3))
+h = llsa.LLSAHandle(llsa.LLSAConfig(n, 64, 16, 8, 3, 3), units)
+out = torch.empty(units, n, 64, device="cuda")
+lib = llsa._lib.load()
+buf = (C.c_ulonglong * 8192)()
+for it in range(2):
+    lib.llsa_debug_trace(buf, 8192)  # reset
+    h.forward(q, k, v, out)
+    torch.cuda.synchronize()
+cnt = lib.llsa_debug_trace(buf, 8192)
+ev = []
+for idx, x in enumerate(buf[:cnt]):
+    if x >> 63:
+        ev.append((idx // 1024, (idx // 32) % 32, idx % 32, x & 0x7FFFFFFFFFFFFFFF))
+t0 = min(e[3] for e in ev)
+names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"}
+ev.sort(key=lambda e: e[3])
+for r, t, e, c in ev:
+    if t < 8:
+        print(f"{c - t0:>9} {names.get(r, r):>6} tile {t:3d} ev {e}")
