@@ -30,6 +30,7 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -74,6 +75,7 @@ struct TcParams {
   // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
   // shallower ones (gain B^l small) use hi only.
   uint32_t hilo_level;
+  uint32_t dbg;    // debug toggles (LLSA_DBG)
   uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
@@ -1662,6 +1664,81 @@ __global__ void __launch_bounds__(320, 1)
 // The producer and MMA warps take the lowest warp ids: the scheduler favours
 // older warps, and starving the single-thread roles stalls the whole tile.
 // Replaces P/src/attention.cpp:166-214 for the tensor-core shapes.
+// Fine part of the forward (one 16-query fine block x one 16-key block) with
+// a lazily rescaled online softmax: the running reference max m only moves
+// when a block's max exceeds it by more than kLazy (log2 units), so P stays
+// <= 2^kLazy and the O rescale (32 FMUL) is skipped for most blocks; the
+// true row max is tracked separately for ForwardState.  l accumulates on the
+// tensor core (P times a ones column).
+struct FineState {
+  float o[8][4];
+  float lo[4];           // l in an m16n8 accumulator (column 0 of each row pair)
+  float m[2], mt[2];     // reference max, true max (log2 units)
+};
+constexpr float kLazy = 8.f;
+__device__ __forceinline__ void attend_fine(uint32_t kT, uint32_t vT, float bias, float c,
+                                            const uint32_t (&qf)[4][4], uint32_t lane,
+                                            FineState& st) {
+  float s[2][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[j][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t b[4];
+    ldb(kT, 0, ks, lane, b);
+    mma16816(s[0], qf[ks], b[0], b[1]);
+    mma16816(s[1], qf[ks], b[2], b[3]);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[h][i] = fmaf(s[h][i], c, bias);
+  float mx0 = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
+  float mx1 = fmaxf(fmaxf(s[0][2], s[0][3]), fmaxf(s[1][2], s[1][3]));
+  mx0 = quad_max(mx0);
+  mx1 = quad_max(mx1);
+  st.mt[0] = fmaxf(st.mt[0], mx0);
+  st.mt[1] = fmaxf(st.mt[1], mx1);
+  if (__any_sync(0xffffffffu, mx0 > st.m[0] + kLazy || mx1 > st.m[1] + kLazy)) {
+    const float mn0 = fmaxf(st.m[0], mx0), mn1 = fmaxf(st.m[1], mx1);
+    const float a0 = ex2(st.m[0] - mn0), a1 = ex2(st.m[1] - mn1);
+    st.m[0] = mn0;
+    st.m[1] = mn1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      st.o[j][0] *= a0;
+      st.o[j][1] *= a0;
+      st.o[j][2] *= a1;
+      st.o[j][3] *= a1;
+    }
+    st.lo[0] *= a0;
+    st.lo[1] *= a0;
+    st.lo[2] *= a1;
+    st.lo[3] *= a1;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    s[h][0] = ex2(s[h][0] - st.m[0]);
+    s[h][1] = ex2(s[h][1] - st.m[0]);
+    s[h][2] = ex2(s[h][2] - st.m[1]);
+    s[h][3] = ex2(s[h][3] - st.m[1]);
+  }
+  const uint32_t a[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]),
+                         pack_bf16(s[1][0], s[1][1]), pack_bf16(s[1][2], s[1][3])};
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn) {
+    uint32_t b[4];
+    ldb_t(vT, 0, dn * 16, lane, b);
+    mma16816(st.o[2 * dn], a, b[0], b[1]);
+    mma16816(st.o[2 * dn + 1], a, b[2], b[3]);
+  }
+  // row sums of P: B = ones in column n = 0 (lanes with n = lane >> 2 == 0)
+  const uint32_t one = (lane >> 2) == 0 ? 0x3F803F80u : 0u;
+  mma16816(st.lo, a, one, one);
+}
+
 namespace fw5 {
 constexpr int kQBytes = kTileQ * 128;           // 16 KB
 constexpr int kKRing = 3;                       // K' ring: hi + lo of 64 keys
@@ -1669,8 +1746,9 @@ constexpr int kKStage = 16384;
 constexpr int kVRing = 2;                       // V' ring: hi of 64 keys
 constexpr int kVStage = 8192;
 constexpr int kPBytes = kTileQ * 128;           // 128 rows x 64 keys bf16
-constexpr int kFineStages = 3;
+constexpr int kFineStages = 2;
 constexpr int kQStages = 1;
+constexpr int kOfStride = 68;                   // fp32 O_f staging row stride (floats)
 constexpr int kFineWarp = kFineStages * 4096;   // per fine warp: {K, V} blocks
 constexpr int kMaxChunks = 6;
 constexpr int kOffQ = 0;
@@ -1678,14 +1756,17 @@ constexpr int kOffK = kOffQ + kQStages * kQBytes;      // 16 KB
 constexpr int kOffV = kOffK + kKRing * kKStage;        // 64 KB
 constexpr int kOffP = kOffV + kVRing * kVStage;        // 80 KB
 constexpr int kOffFine = kOffP + 2 * kPBytes;          // 112 KB
-constexpr int kOffStat = kOffFine + 8 * kFineWarp;     // 208 KB
-constexpr int kOffEnt = kOffStat + 2 * 2 * kTileQ * 4; // + (m_c, l_c) x 2 tiles
-constexpr int kOffBar = kOffEnt + 512;                 // entry bias[32], chunk info[8], rows[2][32]
+constexpr int kOffOf = kOffFine + 8 * kFineWarp;       // 176 KB: fine partial O_f [128][68]
+constexpr int kOffStat = kOffOf + kTileQ * kOfStride * 4;
+constexpr int kOffEnt = kOffStat + 3 * kTileQ * 4;     // + (m_f, l_f, true max)
+// ones tile (1024-aligned: a SW128 atom): B operand column 64 of the PV MMA (l_c)
+constexpr int kOffOnes = (kOffEnt + 1024 + 1023) & ~1023;  // after bias[32], chunk info, rows[2][32]
+constexpr int kOffBar = kOffOnes + 8192;
 enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 8, VFULL = 12, VEMPTY = 15, SREADY = 18,
-       SFREE = 24, PFULL = 30, PEMPTY = 32, OREADY = 34, OFREE = 36, CDONE = 38, CFREE = 40,
-       NBAR = 42 };
+       SFREE = 24, PFULL = 30, PEMPTY = 32, OREADY = 34, OFREE = 36, FDONE = 38, FFREE = 39,
+       NBAR = 40 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
-constexpr int kThreads = 15 * 32;  // 0 K'+Q TMA, 1 MMA, 2 V' TMA, 3-6 coarse, 7-14 fine
+constexpr int kThreads = 16 * 32;  // 0 K' gather, 1 MMA, 2 V' gather, 3-6 coarse, 7-14 fine, 15 Q TMA
 constexpr uint32_t kTmemCols = 512;  // S: [0, 384), O: 384 + 64·buffer
 constexpr uint32_t kMaxEntries = 4 * kMaxChunks;
 }  // namespace fw5
@@ -1700,7 +1781,8 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
-  float* cstat = reinterpret_cast<float*>(smem + kOffStat);  // [2][m | l][128]
+  float* fstat = reinterpret_cast<float*>(smem + kOffStat);  // [m_f | l_f][128]
+  float* ofs = reinterpret_cast<float*>(smem + kOffOf);      // O_f [128][kOfStride]
   const uint64_t tpu = p.n / kTileQ;
   const uint64_t total = tpu * units;
   const uint32_t nce = p.nce, nch = (nce + 3) / 4;
@@ -1719,6 +1801,18 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
   uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 256);  // [K | V][32]
   if (tid < nce) ent_bias[tid] = p.bias2[entry_level(p, tid)];
   if (tid < nch) ch_info[tid] = chunk_ne(tid) | (chunk_lo(tid) ? 0x100u : 0u);
+  // a [64 keys][64] MN-major SW128 tile whose column 0 is 1.0: the second N
+  // block of the PV MMA's B operand, so TMEM column 64 of O_c accumulates l_c
+  for (uint32_t x = tid; x < 64 * 8; x += blockDim.x) {
+    const uint32_t kr = x >> 3, c = x & 7;
+    const uint32_t v = c == (kr & 7) ? 0x3F80u : 0u;  // logical chunk 0 of row kr
+    *reinterpret_cast<uint4*>(smem + kOffOnes + kr * 128 + c * 16) = make_uint4(v, 0, 0, 0);
+  }
+  fence_proxy_async();
+  // TMEM: S chunks at [0, 64·nch); O_c buffers (80 columns: O and l_c) after
+  const uint32_t o_base = 64 * nch;
+  const uint32_t nob = o_base + 2 * 96 <= kTmemCols ? 2u : 1u;
+  const uint32_t o_stride = 96;
   if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -1728,8 +1822,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       mbar_init(bar(PEMPTY + i), 1);
       mbar_init(bar(OREADY + i), 1);
       mbar_init(bar(OFREE + i), 128);
-      mbar_init(bar(CDONE + i), 128);
-      mbar_init(bar(CFREE + i), 256);
     }
     for (int i = 0; i < kKRing; ++i) {
       mbar_init(bar(KFULL + i), 1);
@@ -1743,6 +1835,8 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       mbar_init(bar(SREADY + i), 1);
       mbar_init(bar(SFREE + i), 128);
     }
+    mbar_init(bar(FDONE), 256);
+    mbar_init(bar(FFREE), 128);
     fence_mbar_init();
   }
   fence_before();
@@ -1756,13 +1850,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
     // resolves the tile's coarse rows itself, so the K' side runs ahead of
     // the PV side by as many tiles as its ring allows.
     const bool kside = warp == 0;
-    if (lane == 0) {
-      prefetch_map(kside ? &m.q : &m.vhi);
-      if (kside) {
-        prefetch_map(&m.khi);
-        prefetch_map(&m.klo);
-      }
-    }
     // The coarse rows are gathered with cp.async by all 32 lanes (16 B per
     // lane per instruction; a 2 KB entry is 4 per lane) into the 128-byte
     // swizzled layout the UMMA descriptors expect; a chunk is published
@@ -1770,6 +1857,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
     // one chunk behind the issue front.  Per-entry TMA boxes were issue-bound
     // here (~150 cycles per 2 KB box).
     const uint32_t ring = kside ? kKRing : kVRing;
+    const Block16Lane bl = block16_lane(lane);
     uint32_t* rows = ent_rows + (kside ? 0 : 32);
     const bf16* arr0 = kside ? p.khi : p.vhi;
     const bf16* arr1 = p.klo;
@@ -1784,13 +1872,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       }
       __syncwarp();
       if (lane == 0) trace_ev(p, kside ? 1 : 2, i, 0);
-      if (kside && lane == 0) {
-        const uint32_t qs = i % kQStages;
-        if (i >= (uint32_t)kQStages) mbar_wait(bar(QEMPTY + qs), ((i / kQStages) - 1) & 1);
-        mbar_expect_tx(bar(QFULL + qs), kQBytes);
-        tma_load_2d(sbase + kOffQ + qs * kQBytes, &m.q, 0, (int)(unit * p.n + q0),
-                    bar(QFULL + qs));
-      }
       uint32_t prev_full = 0;
       for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
         const uint32_t s = rc % ring;
@@ -1800,12 +1881,8 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         const uint32_t dst = sbase + (kside ? kOffK + s * kKStage : kOffV + s * kVStage);
         for (uint32_t e = 0; e < ne; ++e) {
           const uint64_t row = rows[ch * 4 + e];
-#pragma unroll
-          for (int k4 = 0; k4 < 4; ++k4) {
-            const uint32_t seg = lane + 32 * k4, r = seg >> 3, c = seg & 7;
-            cp_async16(dst + swz(e * 16 + r, c), arr0 + (row + r) * kD + c * 8);
-            if (lo) cp_async16(dst + 8192 + swz(e * 16 + r, c), arr1 + (row + r) * kD + c * 8);
-          }
+          load_block16_async(dst + e * 2048, arr0 + row * kD, bl, lane);
+          if (lo) load_block16_async(dst + 8192 + e * 2048, arr1 + row * kD, bl, lane);
         }
         cp_async_commit();
         if (prev_full) {
@@ -1822,15 +1899,32 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       __syncwarp();
       if (lane == 0 && prev_full) mbar_arrive(prev_full);
     }
+  } else if (warp == 15) {
+    // ------------------------------------------------------------ Q producer
+    // Q(i+1) is issued as soon as tile i's S MMAs and fine warps release the
+    // buffer, independent of the coarse K'/V' rings.
+    if (lane == 0) {
+      prefetch_map(&m.q);
+      uint32_t i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t unit = (uint32_t)(id / tpu);
+        const uint64_t q0 = (id % tpu) * kTileQ;
+        const uint32_t qs = i % kQStages;
+        if (i >= (uint32_t)kQStages) mbar_wait(bar(QEMPTY + qs), ((i / kQStages) - 1) & 1);
+        mbar_expect_tx(bar(QFULL + qs), kQBytes);
+        tma_load_2d(sbase + kOffQ + qs * kQBytes, &m.q, 0, (int)(unit * p.n + q0),
+                    bar(QFULL + qs));
+      }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // S chunk c of tile i reuses TMEM columns [64c, 64c+64) as soon as the
     // coarse warps have read chunk c of tile i-1 (per-chunk SREADY / SFREE).
     if (lane == 0) {
-      const uint32_t idesc_o = idesc_bf16(128, kD, false, true);
+      const uint32_t idesc_o = idesc_bf16(128, kD + 16, false, true);  // O | l_c
       uint32_t kc = 0, vc = 0, pc = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-        const uint32_t qs = i % kQStages, ob = i & 1;
+        const uint32_t qs = i % kQStages, ob = i % nob;
         mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
         const uint32_t sq = sbase + kOffQ + qs * kQBytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
@@ -1854,8 +1948,8 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           trace_ev(p, 3, i, ch);
         }
         commit(bar(QEMPTY + qs));
-        if (i >= 2) mbar_wait(bar(OFREE + ob), ((i >> 1) - 1) & 1);
-        const uint32_t tO = tmem + 384 + 64 * ob;
+        if (i >= nob) mbar_wait(bar(OFREE + ob), ((i / nob) - 1) & 1);
+        const uint32_t tO = tmem + o_base + o_stride * ob;
         for (uint32_t ch = 0; ch < nch; ++ch, ++vc, ++pc) {
           const uint32_t s = vc % kVRing, ps = pc & 1;
           mbar_wait(bar(VFULL + s), (vc / kVRing) & 1);
@@ -1864,9 +1958,10 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           const uint32_t ne = chunk_ne(ch);
           const uint32_t sp = sbase + kOffP + ps * kPBytes;
           const uint32_t sv = sbase + kOffV + s * kVStage;
+          const uint32_t ones_lbo = sbase + kOffOnes - sv;
           for (uint32_t ks = 0; ks < ne; ++ks)
             mma_bf16(tO, desc_kmajor(sp + ks * kKStepKMajor),
-                     desc_mnmajor(sv + ks * kKStepMNMajor, 8192), idesc_o, (ch | ks) > 0);
+                     desc_mnmajor(sv + ks * kKStepMNMajor, ones_lbo), idesc_o, (ch | ks) > 0);
           commit(bar(VEMPTY + s));
           commit(bar(PEMPTY + ps));
           trace_ev(p, 3, i, 16 + ch);
@@ -1911,7 +2006,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       }
       if (tid == 96) trace_ev(p, 4, i, 0);
       // pass 2: P = exp2(s·c + b − m_c) → bf16 ring; l_c
-      float lsum = 0.f;
       for (uint32_t ch = 0; ch < nch; ++ch, ++pc) {
         const uint32_t ne = chunk_ne(ch), ps = pc & 1;
         if (pc >= 2) mbar_wait(bar(PEMPTY + ps), ((pc >> 1) - 1) & 1);
@@ -1935,7 +2029,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
                     const int i0 = ee * 16 + half * 8 + k * 2;
                     const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
                     const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
-                    lsum += p0 + p1;
                     pk[k] = pack_bf16(p0, p1);
                   }
                   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
@@ -1951,31 +2044,52 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         fence_proxy_async();
         mbar_arrive(bar(PFULL + ps));
       }
-      // O_c (raw) → out; (m_c, l_c) → smem for the fine warps' merge
-      const uint32_t ob = i & 1;
+      // epilogue: merge with the fine partition of the same rows (staged in
+      // smem by the fine warps), O = (O_c 2^(m_c-m) + O_f 2^(m_f-m)) / l
+      const uint32_t ob = i % nob;
       if (tid == 96) trace_ev(p, 4, i, 1);
-      mbar_wait(bar(OREADY + ob), (i >> 1) & 1);
+      mbar_wait(bar(OREADY + ob), (i / nob) & 1);
+      mbar_wait(bar(FDONE), i & 1);
       if (tid == 96) trace_ev(p, 4, i, 2);
       fence_after();
-      float* o = p.out + (uint64_t)unit * p.n * kD + (q0 + row) * kD;
+      const uint32_t tO = tmem + lane_off + o_base + o_stride * ob;
+      uint32_t lraw;
+      tmem_ld1(tO + kD, lraw);
+      tmem_ld_wait();
+      const float lsum = __uint_as_float(lraw);
+      const float mf = fstat[row], lf = fstat[kTileQ + row];
+      const float mrow = fmaxf(mx, fstat[2 * kTileQ + row]);  // the true row max
+      const float ac = ex2(mx - mrow), af = ex2(mf - mrow);
+      const float lt = lsum * ac + lf * af;
+      const float inv = 1.f / lt;
+      const float sc = ac * inv, sf = af * inv;
+      const uint64_t ro = (uint64_t)unit * p.n + q0 + row;
+      float* o = p.out + ro * kD;
+      const float* of = ofs + row * kOfStride;
+      bool bad = !(lt > 0.f) || !isfinite(lt);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t ov[32];
-        tmem_ld32(tmem + lane_off + 384 + 64 * ob + 32 * hh, ov);
+        tmem_ld32(tO + 32 * hh, ov);
         tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          reinterpret_cast<float4*>(o + 32 * hh)[k] =
-              make_float4(__uint_as_float(ov[4 * k]), __uint_as_float(ov[4 * k + 1]),
-                          __uint_as_float(ov[4 * k + 2]), __uint_as_float(ov[4 * k + 3]));
+        for (int k = 0; k < 8; ++k) {
+          const float4 f = *reinterpret_cast<const float4*>(of + 32 * hh + 4 * k);
+          float4 v;
+          v.x = __uint_as_float(ov[4 * k]) * sc + f.x * sf;
+          v.y = __uint_as_float(ov[4 * k + 1]) * sc + f.y * sf;
+          v.z = __uint_as_float(ov[4 * k + 2]) * sc + f.z * sf;
+          v.w = __uint_as_float(ov[4 * k + 3]) * sc + f.w * sf;
+          bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+          reinterpret_cast<float4*>(o + 32 * hh)[k] = v;
+        }
       }
       fence_before();
       mbar_arrive(bar(OFREE + ob));
-      if (i >= 2) mbar_wait(bar(CFREE + ob), ((i >> 1) - 1) & 1);
-      cstat[ob * 256 + row] = mx;
-      cstat[ob * 256 + 128 + row] = lsum;
-      __threadfence_block();
-      mbar_arrive(bar(CDONE + ob));
+      mbar_arrive(bar(FFREE));
+      p.row_max[ro] = mrow / kLog2e;
+      p.row_denom[ro] = lt;
+      if (__any_sync(0xffffffffu, bad) && lane == 0) raise_flag(p.flag, llsa_dev::kErrNonFinite);
       if (tid == 96) trace_ev(p, 4, i, 3);
     }
   } else {
@@ -1985,36 +2099,47 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
     const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
     const uint64_t nfb = p.n / kBS;
     const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
+    const Block16Lane bl = block16_lane(lane);
+    // the warp's K fine block ids of a tile, one per lane (K <= 32 on this
+    // path); the next tile's are fetched while this one computes
+    auto fine_ids = [&](uint64_t id) -> uint32_t {
+      if (id >= total || lane >= p.K) return 0u;
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t fb = (id % tpu) * (kTileQ / kBS) + fw;
+      return p.tables[(uint64_t)unit * p.table_entries + p.table_off[0] + fb * p.K + lane];
+    };
+    uint32_t next_ids = fine_ids(blockIdx.x);
     uint32_t i = 0;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint64_t q0 = (id % tpu) * kTileQ;
       const uint32_t qs = i % kQStages;
       const uint64_t in_off = (uint64_t)unit * p.n * kD;
-      const uint32_t* frow =
-          p.tables + (uint64_t)unit * p.table_entries + p.table_off[0] + (q0 / kBS + fw) * p.K;
+      const uint32_t myb = next_ids;
       auto load_fine = [&](uint32_t j) {
-        uint32_t b = frow[j];
+        uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
         if (b >= nfb) {
           raise_flag(p.flag, llsa_dev::kErrIndex);
           b = 0;
         }
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
-        load_rows_async(base + kTile16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+        load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
       };
 #pragma unroll
       for (uint32_t j = 0; j + 1 < (uint32_t)kFineStages; ++j) {
         if (j < p.K) load_fine(j);
         cp_async_commit();
       }
-      SoftmaxState st;
+      next_ids = fine_ids(id + gridDim.x);
+      FineState st;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) st.o[j][e] = 0.f;
-      st.m[0] = st.m[1] = -INFINITY;
-      st.l[0] = st.l[1] = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) st.lo[e] = 0.f;
+      st.m[0] = st.m[1] = st.mt[0] = st.mt[1] = -INFINITY;
       uint32_t qf[4][4];
       if (tid == 224) trace_ev(p, 5, i, 0);
       mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
@@ -2030,48 +2155,35 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         cp_async_wait<kFineStages - 1>();
         __syncwarp();
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        attend_fwd<false>(base, base, base + kTile16, 0, 1, bf, bf, c2, qf, lane, st);
+        attend_fine(base, base + kTile16, bf, c2, qf, lane, st);
         __syncwarp();
       }
-      // merge with the coarse partition of the same rows
-      const uint32_t ob = i & 1;
+      // publish the fine partition (raw O_f, m_f, l_f) for the coarse warps
       if (tid == 224) trace_ev(p, 5, i, 1);
-      mbar_wait(bar(CDONE + ob), (i >> 1) & 1);
+      if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
       if (tid == 224) trace_ev(p, 5, i, 2);
-      const float lf0 = quad_sum(st.l[0]), lf1 = quad_sum(st.l[1]);
-      const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
-      const float mc0 = cstat[ob * 256 + r0], mc1 = cstat[ob * 256 + r1];
-      const float lc0 = cstat[ob * 256 + 128 + r0], lc1 = cstat[ob * 256 + 128 + r1];
-      __syncwarp();
-      mbar_arrive(bar(CFREE + ob));
-      const float m0 = fmaxf(st.m[0], mc0), m1 = fmaxf(st.m[1], mc1);
-      const float af0 = ex2(st.m[0] - m0), ac0 = ex2(mc0 - m0);
-      const float af1 = ex2(st.m[1] - m1), ac1 = ex2(mc1 - m1);
-      const float l0 = lf0 * af0 + lc0 * ac0, l1 = lf1 * af1 + lc1 * ac1;
-      const float i0 = 1.f / l0, i1 = 1.f / l1;
-      float* o0 = p.out + in_off + (q0 + r0) * kD;
-      float* o1 = p.out + in_off + (q0 + r1) * kD;
-      bool bad = !(l0 > 0.f) || !(l1 > 0.f) || !isfinite(l0) || !isfinite(l1);
+      {
+        // l of rows r, r + 8 sits in column 0 of the l accumulator (lane & 3 == 0)
+        const float lf0 = __shfl_sync(0xffffffffu, st.lo[0], lane & ~3u);
+        const float lf1 = __shfl_sync(0xffffffffu, st.lo[2], lane & ~3u);
+        const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
+        float* o0 = ofs + r0 * kOfStride;
+        float* o1 = ofs + r1 * kOfStride;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float2 c0 = __ldcg(reinterpret_cast<const float2*>(o0 + j * 8 + cc));
-        const float2 c1 = __ldcg(reinterpret_cast<const float2*>(o1 + j * 8 + cc));
-        const float2 v0 = make_float2((st.o[j][0] * af0 + c0.x * ac0) * i0,
-                                      (st.o[j][1] * af0 + c0.y * ac0) * i0);
-        const float2 v1 = make_float2((st.o[j][2] * af1 + c1.x * ac1) * i1,
-                                      (st.o[j][3] * af1 + c1.y * ac1) * i1);
-        bad |= !isfinite(v0.x) || !isfinite(v0.y) || !isfinite(v1.x) || !isfinite(v1.y);
-        *reinterpret_cast<float2*>(o0 + j * 8 + cc) = v0;
-        *reinterpret_cast<float2*>(o1 + j * 8 + cc) = v1;
+        for (int j = 0; j < 8; ++j) {
+          *reinterpret_cast<float2*>(o0 + j * 8 + cc) = make_float2(st.o[j][0], st.o[j][1]);
+          *reinterpret_cast<float2*>(o1 + j * 8 + cc) = make_float2(st.o[j][2], st.o[j][3]);
+        }
+        if ((lane & 3) == 0) {
+          fstat[r0] = st.m[0];
+          fstat[r1] = st.m[1];
+          fstat[kTileQ + r0] = lf0;
+          fstat[kTileQ + r1] = lf1;
+          fstat[2 * kTileQ + r0] = st.mt[0];
+          fstat[2 * kTileQ + r1] = st.mt[1];
+        }
       }
-      if ((lane & 3) == 0) {
-        const uint64_t ro = (uint64_t)unit * p.n + q0;
-        p.row_max[ro + r0] = m0 / kLog2e;
-        p.row_max[ro + r1] = m1 / kLog2e;
-        p.row_denom[ro + r0] = l0;
-        p.row_denom[ro + r1] = l1;
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) raise_flag(p.flag, llsa_dev::kErrNonFinite);
+      mbar_arrive(bar(FDONE));
     }
   }
   fence_before();
@@ -2123,7 +2235,8 @@ bool fwd5_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   const char* f = getenv("LLSA_FWD5");
   const uint32_t nce = coarse_entries(g);
-  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries;
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries &&
+         g.K <= 32;
 }
 
 void rows_layout(const Geometry& g, TcParams& P) {
@@ -2200,6 +2313,8 @@ TcParams make_params(const Geometry& g) {
     P.csc_flat_off[l] = g.csc_flat_off[l];
   }
   P.flag = device_flag();
+  const char* dg = getenv("LLSA_DBG");
+  P.dbg = dg ? (uint32_t)atoi(dg) : 0u;
   const char* tr = getenv("LLSA_TRACE");
   P.trace = tr && tr[0] == '1' ? 1u : 0u;
   const char* hl = getenv("LLSA_HILO_LEVEL");  // 1: hi + lo on every coarse level

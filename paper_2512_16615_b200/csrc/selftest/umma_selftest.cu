@@ -18,12 +18,12 @@ __device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t col) {
 
 __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
                                                        const __nv_bfloat16* b, float* d,
-                                                       int N, int a_mn, int b_mn) {
+                                                       int N, int a_mn, int b_mn, int b_lbo) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;                 // 16 KB
-  uint8_t* sB = smem + 16384;         // up to 16 KB
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 32768);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 32768 + 8);
+  uint8_t* sB = smem + 16384;         // MN-major: N blocks b_lbo bytes apart
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 16384 + 65536);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 16384 + 65536 + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // A: logical [128 m][64 k]; K-major: rows m; MN-major: rows k, 64-wide m blocks 8 KB apart
   for (int e = tid; e < 128 * 64; e += 128) {
@@ -36,11 +36,11 @@ __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
   for (int e = tid; e < N * 64; e += 128) {
     const int n = e / 64, k = e % 64;
     const __nv_bfloat16 v = b_mn ? b[k * N + n] : b[n * 64 + k];
-    const uint32_t off = b_mn ? (n / 64) * 8192 + tile_off(k, n % 64) : tile_off(n, k);
+    const uint32_t off = b_mn ? (n / 64) * b_lbo + tile_off(k, n % 64) : tile_off(n, k);
     *reinterpret_cast<__nv_bfloat16*>(sB + off) = v;
   }
   fence_proxy_async();
-  const uint32_t ncols = N <= 64 ? 64 : 128;
+  const uint32_t ncols = N <= 64 ? 64 : N <= 128 ? 128 : 256;
   if (warp == 0) tmem_alloc(llsa_tc::smem_u32(tslot), ncols);
   if (tid == 0) {
     mbar_init(llsa_tc::smem_u32(mbar), 1);
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
     for (int ks = 0; ks < 4; ++ks) {
       const uint64_t ad = a_mn ? desc_mnmajor(A + ks * kKStepMNMajor, 8192)
                                : desc_kmajor(A + ks * kKStepKMajor);
-      const uint64_t bd = b_mn ? desc_mnmajor(B + ks * kKStepMNMajor, 8192)
+      const uint64_t bd = b_mn ? desc_mnmajor(B + ks * kKStepMNMajor, b_lbo)
                                : desc_kmajor(B + ks * kKStepKMajor);
       mma_bf16(tmem, ad, bd, idesc, ks > 0);
     }
@@ -64,11 +64,12 @@ __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
   }
   mbar_wait(llsa_tc::smem_u32(mbar), 0);
   fence_after();
-  for (int c = 0; c < N / 32; ++c) {
+  for (int c = 0; c < (N + 31) / 32; ++c) {
     uint32_t r[32];
     tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + c * 32, r);
     tmem_ld_wait();
-    for (int i = 0; i < 32; ++i) d[(32 * warp + lane) * N + c * 32 + i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 32 && c * 32 + i < N; ++i)
+      d[(32 * warp + lane) * N + c * 32 + i] = __uint_as_float(r[i]);
   }
   fence_before();
   __syncthreads();
@@ -78,12 +79,12 @@ __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
 }  // namespace
 
 extern "C" int llsa_umma_selftest(const void* a, const void* b, float* d, int N, int a_mn,
-                                  int b_mn, void* stream) {
-  if (N != 64 && N != 128) return 1;
-  const int smem = 32768 + 64;
+                                  int b_mn, int b_lbo, void* stream) {
+  if (N % 16 || N < 16 || N > 128 || b_lbo % 1024 || b_lbo < 8192 || b_lbo > 32768) return 1;
+  const int smem = 16384 + 65536 + 64;
   cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   selftest_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b), d, N, a_mn,
-      b_mn);
+      b_mn, b_lbo);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

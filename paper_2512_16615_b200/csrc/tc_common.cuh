@@ -39,6 +39,27 @@ __device__ __forceinline__ void load_rows_async(uint32_t tile, uint32_t row0,
   }
 }
 
+// Per-lane constants for load_block16_async: the swizzled offsets of this
+// lane's 16-byte chunk in rows (lane >> 3) + 4k, k even / odd.
+struct Block16Lane {
+  uint32_t even, odd;
+};
+__device__ __forceinline__ Block16Lane block16_lane(uint32_t lane) {
+  const uint32_t r = lane >> 3, sw = (lane & 7) ^ r;
+  return {r * 128u + (sw << 4), r * 128u + ((sw ^ 4u) << 4)};
+}
+// One warp copies a 16-row block (16 x 128 B, contiguous in global) into a
+// swizzled tile at `dst` (the address of the block's first row, row index a
+// multiple of 8): four 16-byte cp.async per lane at precomputed offsets.
+__device__ __forceinline__ void load_block16_async(uint32_t dst, const void* g,
+                                                   const Block16Lane& o, uint32_t lane) {
+  const char* src = reinterpret_cast<const char*>(g) + lane * 16;
+  cp_async16(dst + o.even, src);
+  cp_async16(dst + 512 + o.odd, src + 512);
+  cp_async16(dst + 1024 + o.even, src + 1024);
+  cp_async16(dst + 1536 + o.odd, src + 1536);
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1,
                                         uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"

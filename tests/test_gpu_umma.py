@@ -15,10 +15,11 @@ SO = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                   "paper_2512_16615_b200", "build", "libllsa_umma_selftest.so")
 
 
-@pytest.mark.parametrize("n", [64, 128])
+@pytest.mark.parametrize("n,lbo", [(64, 8192), (128, 8192), (80, 8192), (80, 24576),
+                                   (128, 16384)])
 @pytest.mark.parametrize("a_mn", [0, 1])
 @pytest.mark.parametrize("b_mn", [0, 1])
-def test_umma_gemm(n, a_mn, b_mn):
+def test_umma_gemm(n, lbo, a_mn, b_mn):
     lib = C.CDLL(SO)
     torch.manual_seed(n + 2 * a_mn + b_mn)
     A = torch.randn(128, 64, device="cuda").to(torch.bfloat16)   # [m][k]
@@ -27,7 +28,7 @@ def test_umma_gemm(n, a_mn, b_mn):
     b_in = B.contiguous() if b_mn else B.t().contiguous()         # K-major: [n][k]
     d = torch.empty(128, n, device="cuda")
     rc = lib.llsa_umma_selftest(C.c_void_p(a_in.data_ptr()), C.c_void_p(b_in.data_ptr()),
-                                C.c_void_p(d.data_ptr()), n, a_mn, b_mn,
+                                C.c_void_p(d.data_ptr()), n, a_mn, b_mn, lbo,
                                 C.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert rc == 0
     torch.cuda.synchronize()
