@@ -496,18 +496,19 @@ __global__ void __launch_bounds__(256, 2) tc_dq_kernel(TcParams p) {
   }
   const uint32_t* frow = tab + p.table_off[0] + fb * p.K;
   const uint64_t nfb = p.n / kBS;
+  const Block16Lane bl = block16_lane(lane);
   auto load_fine = [&](uint32_t j, uint32_t stage) {
     uint32_t b = frow[j];
     if (b >= nfb) b = 0;
     const uint32_t base = sF + stage * kFStage;
-    load_rows_async(base, 0, p.k + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
-    load_rows_async(base + kTile16, 0, p.v + in_off + (uint64_t)b * kBS * kD, kBS, lane, 32);
+    load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
+    load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
   };
   __syncthreads();
 
   const uint64_t qrow0 = q0 + warp * 16;
-  load_rows_async(sF + kFStage, 0, p.q + in_off + qrow0 * kD, kBS, lane, 32);
-  load_rows_async(sF + kFStage + kTile16, 0, p.dout + in_off + qrow0 * kD, kBS, lane, 32);
+  load_block16_async(sF + kFStage, p.q + in_off + qrow0 * kD, bl, lane);
+  load_block16_async(sF + kFStage + kTile16, p.dout + in_off + qrow0 * kD, bl, lane);
   load_fine(0, 0);
   const uint32_t nchunks = (p.nce + 1) / 2;
   if (nchunks)
@@ -698,12 +699,17 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
     load_rows_async(sK + 2 * kTile16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
   }
   const uint64_t ro = (uint64_t)unit * p.n;
+  const Block16Lane bl = block16_lane(lane);
   auto load_chunk = [&](uint64_t cidx, uint32_t stage) {
     const uint64_t row = top ? 0 : seg[cidx / cpr];
     const uint64_t t0 = row * span + (cidx % cpr) * QC;
     const uint32_t base = sQs + stage * Cfg::Stage;
-    load_rows_async(base, 0, p.q + in_off + t0 * kD, QC, lane, 32);
-    load_rows_async(base + Cfg::QTile, 0, p.dout + in_off + t0 * kD, QC, lane, 32);
+#pragma unroll
+    for (int h = 0; h < QC / 16; ++h) {
+      load_block16_async(base + h * kTile16, p.q + in_off + (t0 + 16 * h) * kD, bl, lane);
+      load_block16_async(base + Cfg::QTile + h * kTile16, p.dout + in_off + (t0 + 16 * h) * kD,
+                         bl, lane);
+    }
     constexpr uint32_t nv = QC / 4;  // 16 B vectors of lse2 (then of D)
     if (lane < nv)
       cp_async16(base + 2 * Cfg::QTile + lane * 16, p.lse2 + ro + t0 + lane * 4);
@@ -974,8 +980,8 @@ __global__ void __launch_bounds__(256, rows::Layout<LO>::kMinBlocks)
   auto load_tile = [&](uint32_t j, uint32_t stage) {
     const uint64_t t0 = q_begin + (uint64_t)j * kQT;
     const uint32_t base = sbase + kOffStage + stage * kStageAl;
-    load_rows_async(base, 0, p.q + in_off + t0 * kD, kQT, tid, blockDim.x);
-    load_rows_async(base + kQTile, 0, p.dout + in_off + t0 * kD, kQT, tid, blockDim.x);
+    load_rows_fast<kQT, 256>(base, p.q + in_off + t0 * kD, tid);
+    load_rows_fast<kQT, 256>(base + kQTile, p.dout + in_off + t0 * kD, tid);
     if (tid < 16) cp_async16(base + 2 * kQTile + tid * 16, p.lse2 + ro + t0 + tid * 4);
     else if (tid < 32)
       cp_async16(base + 2 * kQTile + kQT * 4 + (tid - 16) * 16, p.drow + ro + t0 + (tid - 16) * 4);

@@ -60,6 +60,20 @@ __device__ __forceinline__ void load_block16_async(uint32_t dst, const void* g,
   cp_async16(dst + 1536 + o.odd, src + 1536);
 }
 
+// CTA-level variant: NTHR threads (a multiple of 64) copy ROWS contiguous
+// 128-byte rows into a swizzled tile at `dst` (row index a multiple of 8).
+// With NTHR/8 a multiple of 8, a thread's row phase (r & 7) is the same for
+// every chunk it moves, so its swizzled offset is one add per copy.
+template <int ROWS, int NTHR>
+__device__ __forceinline__ void load_rows_fast(uint32_t dst, const void* g, uint32_t tid) {
+  static_assert(NTHR % 64 == 0 && (ROWS * 8) % NTHR == 0, "shape");
+  const uint32_t r = tid >> 3, c = tid & 7;
+  const uint32_t off = r * 128u + ((c ^ (r & 7u)) << 4);
+  const char* src = reinterpret_cast<const char*>(g) + tid * 16;
+#pragma unroll
+  for (int k = 0; k < ROWS * 8 / NTHR; ++k) cp_async16(dst + off + k * NTHR * 16, src + k * NTHR * 16);
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1,
                                         uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
