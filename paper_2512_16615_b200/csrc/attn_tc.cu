@@ -2197,6 +2197,422 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// backward dQ — persistent, warp-specialised, fine + coarse in one pass
+// ---------------------------------------------------------------------------
+// The query-major half of the mask-free backward (attention_grad.cpp:16-25,
+// 229-257) for 128-query tiles, structured like tc5_fwd_kernel:
+//   warp 15 (1 lane)  TMA: Q and dO tiles (single buffer)
+//   warp 0            cp.async gather of the coarse K'/V' chunks (hi [+ lo],
+//                     64 keys) → 2-stage ring
+//   warp 1 (1 lane)   MMA: S = Q K'^T, dP = dO V'^T per chunk → TMEM (double
+//                     buffer); dQ_c += dS K'_hi → TMEM (double buffer / tile)
+//   warps 3-6         coarse, thread = query row: dS = P∘(dP − D) with
+//                     P = exp2(S c + b − lse) → bf16 smem ring; at the end of a
+//                     tile dq = scale (dQ_c + dQ_f), written once
+//   warps 7-14        fine, warp 7+w = fine block w on mma.sync; they also
+//                     produce D = rowsum(dO∘O) and the log2 LSE of their rows
+//                     (smem for the coarse warps, global for the kv kernels)
+namespace dqf {
+constexpr int kTileBytes = kTileQ * 128;        // 16 KB
+constexpr int kCStage = 4 * 8192;               // Khi, Klo, Vhi, Vlo of 64 keys
+constexpr int kCRing = 2;
+constexpr int kDSBytes = kTileQ * 128;          // dS chunk: 128 rows x 64 keys bf16
+constexpr int kFineWarp = 2 * 4096;             // 2 stages of one {K, V} block
+constexpr int kOffQ = 0, kOffG = kTileBytes;
+constexpr int kOffC = 2 * kTileBytes;                     // 32 KB
+constexpr int kOffDS = kOffC + kCRing * kCStage;          // 96 KB
+constexpr int kOffFine = kOffDS + 2 * kDSBytes;           // 128 KB
+constexpr int kOffDQf = kOffFine + 8 * kFineWarp;         // 192 KB: dQ_f [128][64] fp32
+constexpr int kOffStat = kOffDQf + kTileQ * kD * 4;       // 224 KB: lse, D x 2 tiles
+constexpr int kOffEnt = kOffStat + 4 * kTileQ * 4;        // bias[32], chunk info[8], rows[32]
+constexpr int kOffBar = kOffEnt + 256;
+enum { QFULL = 0, QEMPTY = 1, KFULL = 2, KEMPTY = 4, SREADY = 6, TFREE = 8, DSREADY = 10,
+       DSFREE = 12, DQREADY = 14, DQFREE = 16, DREADY = 18, FDONE = 20, FFREE = 21,
+       NBAR = 22 };
+constexpr int kSmem = kOffBar + NBAR * 8 + 16;
+constexpr int kThreads = 16 * 32;
+constexpr uint32_t kTmemCols = 512;  // S/dP x 2 buffers [0, 256), dQ_c x 2 [256, 384)
+constexpr uint32_t kMaxEntries = 24;  // ent_rows[24]
+}  // namespace dqf
+
+// fp32 [128][64] staging with 8-float groups XOR-swizzled by row (conflict-free
+// row-wise float4 reads, 2-way fragment writes)
+__device__ __forceinline__ uint32_t dqf_idx(uint32_t row, uint32_t col) {
+  return row * 64u + (col ^ ((row & 7u) << 3));
+}
+
+__global__ void __launch_bounds__(dqf::kThreads, 1)
+    tc5_dqf_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TmaMaps m,
+                   uint32_t units) {
+  using namespace llsa_umma;
+  using namespace dqf;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
+  float* stat = reinterpret_cast<float*>(smem + kOffStat);  // [2 tiles][lse | D][128]
+  float* dqs = reinterpret_cast<float*>(smem + kOffDQf);
+  float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
+  uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
+  uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 160);  // [24]
+  const uint64_t tpu = p.n / kTileQ;
+  const uint64_t total = tpu * units;
+  const uint32_t nce = p.nce, nch = (nce + 3) / 4;
+  if (tid < nce) ent_bias[tid] = p.bias2[entry_level(p, tid)];
+  if (tid < nch) {
+    bool lo = false;
+    const uint32_t ne = min(4u, nce - tid * 4);
+    for (uint32_t e = tid * 4; e < tid * 4 + ne; ++e) lo |= entry_level(p, e) >= p.hilo_level;
+    ch_info[tid] = ne | (lo ? 0x100u : 0u);
+  }
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    mbar_init(bar(QFULL), 1);
+    mbar_init(bar(QEMPTY), 1 + 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(KFULL + i), 1);
+      mbar_init(bar(KEMPTY + i), 1);
+      mbar_init(bar(SREADY + i), 1);
+      mbar_init(bar(TFREE + i), 128);
+      mbar_init(bar(DSREADY + i), 128);
+      mbar_init(bar(DSFREE + i), 1);
+      mbar_init(bar(DQREADY + i), 1);
+      mbar_init(bar(DQFREE + i), 128);
+      mbar_init(bar(DREADY + i), 256);
+    }
+    mbar_init(bar(FDONE), 256);
+    mbar_init(bar(FFREE), 128);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const float c2 = p.scale * kLog2e;
+
+  if (warp == 15) {
+    // ------------------------------------------------------------ Q / dO TMA
+    if (lane == 0) {
+      prefetch_map(&m.q);
+      prefetch_map(&m.g);
+      uint32_t i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t unit = (uint32_t)(id / tpu);
+        const uint64_t q0 = (id % tpu) * kTileQ;
+        if (i >= 1) mbar_wait(bar(QEMPTY), (i - 1) & 1);
+        mbar_expect_tx(bar(QFULL), 2 * kTileBytes);
+        tma_load_2d(sbase + kOffQ, &m.q, 0, (int)(unit * p.n + q0), bar(QFULL));
+        tma_load_2d(sbase + kOffG, &m.g, 0, (int)(unit * p.n + q0), bar(QFULL));
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------------ K'/V' gather
+    const Block16Lane bl = block16_lane(lane);
+    uint32_t rc = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      if (lane < nce) {
+        uint32_t l, r;
+        coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, q0 / kBS, lane, l, r);
+        ent_rows[lane] = (uint32_t)(unit * p.pyr_rows) + r;
+      }
+      __syncwarp();
+      uint32_t prev_full = 0;
+      for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
+        const uint32_t s = rc % kCRing;
+        const uint32_t info = ch_info[ch], ne = info & 0xFF;
+        const bool lo = info & 0x100u;
+        if (rc >= (uint32_t)kCRing) {
+          // the slot is released by the dQ MMA two chunks back, which needs the
+          // previous chunk's S/dP first: publish that chunk before blocking
+          if (prev_full) {
+            cp_async_wait<0>();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(prev_full);
+            prev_full = 0;
+          }
+          mbar_wait(bar(KEMPTY + s), ((rc / kCRing) - 1) & 1);
+        }
+        const uint32_t dst = sbase + kOffC + s * kCStage;
+        for (uint32_t e = 0; e < ne; ++e) {
+          const uint64_t o = (uint64_t)ent_rows[ch * 4 + e] * kD;
+          load_block16_async(dst + e * 2048, p.khi + o, bl, lane);
+          load_block16_async(dst + 16384 + e * 2048, p.vhi + o, bl, lane);
+          if (lo) {
+            load_block16_async(dst + 8192 + e * 2048, p.klo + o, bl, lane);
+            load_block16_async(dst + 24576 + e * 2048, p.vlo + o, bl, lane);
+          }
+        }
+        cp_async_commit();
+        if (prev_full) {
+          cp_async_wait<1>();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(prev_full);
+        }
+        prev_full = bar(KFULL + s);
+      }
+      cp_async_wait<0>();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0 && prev_full) mbar_arrive(prev_full);
+      __syncwarp();  // ent_rows is rewritten for the next tile
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc_q = idesc_bf16(128, kD, false, true);
+      struct Prev {
+        uint32_t c, s, ne, first, last, ti;
+      } pv{};
+      bool have = false;
+      auto do_dq = [&](const Prev& x) {
+        const uint32_t b = x.c & 1, tb = x.ti & 1;
+        mbar_wait(bar(DSREADY + b), (x.c >> 1) & 1);
+        if (x.first && x.ti >= 2) mbar_wait(bar(DQFREE + tb), ((x.ti >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t sds = sbase + kOffDS + b * kDSBytes;
+        const uint32_t khi = sbase + kOffC + x.s * kCStage;
+        const uint32_t tq = tmem + 256 + tb * 64;
+        for (uint32_t ks = 0; ks < x.ne; ++ks)
+          mma_bf16(tq, desc_kmajor(sds + ks * kKStepKMajor),
+                   desc_mnmajor(khi + ks * kKStepMNMajor, 8192), idesc_q,
+                   (x.first && ks == 0) ? 0u : 1u);
+        commit(bar(KEMPTY + x.s));
+        commit(bar(DSFREE + b));
+        if (x.last) commit(bar(DQREADY + tb));
+      };
+      uint32_t c = 0, i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        mbar_wait(bar(QFULL), i & 1);
+        const uint32_t sq = sbase + kOffQ, sg = sbase + kOffG;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+          const uint32_t s = c % kCRing, b = c & 1;
+          mbar_wait(bar(KFULL + s), (c / kCRing) & 1);
+          if (c >= 2) mbar_wait(bar(TFREE + b), ((c >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t info = ch_info[ch], ne = info & 0xFF;
+          const bool lo = info & 0x100u;
+          const uint32_t idesc = idesc_bf16(128, 16 * ne, false, false);
+          const uint32_t st = sbase + kOffC + s * kCStage;
+          const uint32_t tS = tmem + b * 128, tP = tS + 64;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t aq = desc_kmajor(sq + ks * kKStepKMajor);
+            const uint64_t ag = desc_kmajor(sg + ks * kKStepKMajor);
+            mma_bf16(tS, aq, desc_kmajor(st + ks * kKStepKMajor), idesc, ks > 0);
+            mma_bf16(tP, ag, desc_kmajor(st + 16384 + ks * kKStepKMajor), idesc, ks > 0);
+            if (lo) {
+              mma_bf16(tS, aq, desc_kmajor(st + 8192 + ks * kKStepKMajor), idesc, 1);
+              mma_bf16(tP, ag, desc_kmajor(st + 24576 + ks * kKStepKMajor), idesc, 1);
+            }
+          }
+          commit(bar(SREADY + b));
+          if (ch + 1 == nch) commit(bar(QEMPTY));
+          if (have) do_dq(pv);
+          pv = Prev{c, s, ne, ch == 0 ? 1u : 0u, ch + 1 == nch ? 1u : 0u, i};
+          have = true;
+        }
+      }
+      if (have) do_dq(pv);
+    }
+  } else if (warp >= 3 && warp < 7) {
+    // ------------------------------------------------------------ coarse warps
+    const uint32_t row = 32 * (warp & 3) + lane;
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    uint32_t c = 0, i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      const uint32_t tb = i & 1;
+      mbar_wait(bar(DREADY + tb), (i >> 1) & 1);
+      const float lse = stat[tb * 256 + row], Drow = stat[tb * 256 + 128 + row];
+      for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+        const uint32_t b = c & 1, ne = ch_info[ch] & 0xFF;
+        mbar_wait(bar(SREADY + b), (c >> 1) & 1);
+        fence_after();
+        if (c >= 2) mbar_wait(bar(DSFREE + b), ((c >> 1) - 1) & 1);
+        const uint32_t sds = sbase + kOffDS + b * kDSBytes;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (2 * hh < (int)ne) {
+            uint32_t sv[32], gv[32];
+            tmem_ld32(tmem + lane_off + b * 128 + 32 * hh, sv);
+            tmem_ld32(tmem + lane_off + b * 128 + 64 + 32 * hh, gv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int ee = 0; ee < 2; ++ee) {
+              const uint32_t e = 2 * hh + ee;
+              if (e < ne) {
+                const float nb = ent_bias[ch * 4 + e] - lse;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                  uint32_t pk[4];
+#pragma unroll
+                  for (int k = 0; k < 4; ++k) {
+                    const int i0 = ee * 16 + half * 8 + k * 2;
+                    const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
+                    const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
+                    pk[k] = pack_bf16(p0 * (__uint_as_float(gv[i0]) - Drow),
+                                      p1 * (__uint_as_float(gv[i0 + 1]) - Drow));
+                  }
+                  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                                   sds + swz(row, e * 2 + half)),
+                               "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+                }
+              }
+            }
+          }
+        }
+        fence_before();
+        mbar_arrive(bar(TFREE + b));
+        fence_proxy_async();
+        mbar_arrive(bar(DSREADY + b));
+      }
+      // tile epilogue: dq = scale (dQ_c + dQ_f), written once
+      mbar_wait(bar(DQREADY + tb), (i >> 1) & 1);
+      mbar_wait(bar(FDONE), i & 1);
+      fence_after();
+      float* d = p.dq + ((uint64_t)unit * p.n + q0 + row) * kD;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t r0[32];
+        tmem_ld32(tmem + lane_off + 256 + tb * 64 + 32 * hh, r0);
+        tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 f =
+              *reinterpret_cast<const float4*>(dqs + dqf_idx(row, 32 * hh + 4 * k));
+          float4 v;
+          v.x = (__uint_as_float(r0[4 * k]) + f.x) * p.scale;
+          v.y = (__uint_as_float(r0[4 * k + 1]) + f.y) * p.scale;
+          v.z = (__uint_as_float(r0[4 * k + 2]) + f.z) * p.scale;
+          v.w = (__uint_as_float(r0[4 * k + 3]) + f.w) * p.scale;
+          reinterpret_cast<float4*>(d + 32 * hh)[k] = v;
+        }
+      }
+      fence_before();
+      mbar_arrive(bar(DQFREE + tb));
+      mbar_arrive(bar(FFREE));
+    }
+  } else if (warp >= 7) {
+    // ------------------------------------------------------------ fine warps
+    const uint32_t fw = warp - 7;
+    const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
+    const uint64_t nfb = p.n / kBS;
+    const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
+    const Block16Lane bl = block16_lane(lane);
+    auto fine_ids = [&](uint64_t id) -> uint32_t {
+      if (id >= total || lane >= p.K) return 0u;
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t fb = (id % tpu) * (kTileQ / kBS) + fw;
+      return p.tables[(uint64_t)unit * p.table_entries + p.table_off[0] + fb * p.K + lane];
+    };
+    uint32_t next_ids = fine_ids(blockIdx.x);
+    const float bf = p.bias2[0];
+    uint32_t i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint64_t q0 = (id % tpu) * kTileQ;
+      const uint64_t in_off = (uint64_t)unit * p.n * kD;
+      const uint32_t myb = next_ids;
+      auto load_fine = [&](uint32_t j) {
+        uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
+        if (b >= nfb) {
+          raise_flag(p.flag, llsa_dev::kErrIndex);
+          b = 0;
+        }
+        const uint32_t base = sF + (j & 1) * 4096;
+        load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
+      };
+      load_fine(0);
+      cp_async_commit();
+      next_ids = fine_ids(id + gridDim.x);
+      // D = rowsum(dO∘O) (fp32 O) and the log2 LSE of this warp's 16 rows;
+      // lane pair (2ρ, 2ρ+1) owns row ρ (columns [32·half, +32))
+      const uint32_t rr = lane >> 1, half = lane & 1;
+      const uint64_t trow = q0 + fw * 16 + rr;
+      const uint64_t ro = (uint64_t)unit * p.n;
+      float4 ov[8];
+      {
+        const float4* o4 = reinterpret_cast<const float4*>(p.out_in + in_off + trow * kD + half * 32);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ov[k] = o4[k];
+      }
+      const float lse_r = p.rm_in[ro + trow] * kLog2e + __log2f(p.rd_in[ro + trow]);
+      mbar_wait(bar(QFULL), i & 1);
+      uint32_t qf[4][4], gf[4][4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        lda(sbase + kOffQ, fw * 16, ks, lane, qf[ks]);
+        lda(sbase + kOffG, fw * 16, ks, lane, gf[ks]);
+      }
+      float dsum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // dO row rr, 16-byte chunks 4·half + k
+        uint4 gv;
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
+                     : "r"(sbase + kOffG + swz(fw * 16 + rr, half * 4 + k)));
+        const uint32_t w[4] = {gv.x, gv.y, gv.z, gv.w};
+        const float of[8] = {ov[2 * k].x, ov[2 * k].y, ov[2 * k].z, ov[2 * k].w,
+                             ov[2 * k + 1].x, ov[2 * k + 1].y, ov[2 * k + 1].z, ov[2 * k + 1].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          dsum = fmaf(__uint_as_float(w[t] << 16), of[2 * t], dsum);
+          dsum = fmaf(__uint_as_float(w[t] & 0xffff0000u), of[2 * t + 1], dsum);
+        }
+      }
+      mbar_arrive(bar(QEMPTY));
+      dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+      const uint32_t tb = i & 1;
+      if (half == 0) {
+        p.drow[ro + trow] = dsum;
+        p.lse2[ro + trow] = lse_r;
+        stat[tb * 256 + fw * 16 + rr] = lse_r;
+        stat[tb * 256 + 128 + fw * 16 + rr] = dsum;
+      }
+      mbar_arrive(bar(DREADY + tb));
+      const float D0 = __shfl_sync(0xffffffffu, dsum, 2 * r);
+      const float D1 = __shfl_sync(0xffffffffu, dsum, 2 * (r + 8));
+      const float lse0 = __shfl_sync(0xffffffffu, lse_r, 2 * r);
+      const float lse1 = __shfl_sync(0xffffffffu, lse_r, 2 * (r + 8));
+      float dq[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dq[j][e] = 0.f;
+      for (uint32_t j = 0; j < p.K; ++j) {
+        if (j + 1 < p.K) load_fine(j + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const uint32_t base = sF + (j & 1) * 4096;
+        attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
+                         lse1, D0, D1, lane, dq);
+        __syncwarp();
+      }
+      // publish the fine part of dQ (unscaled) for the coarse warps' epilogue
+      if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
+      const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        *reinterpret_cast<float2*>(dqs + dqf_idx(r0, j * 8 + cc)) = make_float2(dq[j][0], dq[j][1]);
+        *reinterpret_cast<float2*>(dqs + dqf_idx(r1, j * 8 + cc)) = make_float2(dq[j][2], dq[j][3]);
+      }
+      mbar_arrive(bar(FDONE));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -2242,6 +2658,15 @@ bool fwd5_path(const Geometry& g) {
   const char* f = getenv("LLSA_FWD5");
   const uint32_t nce = coarse_entries(g);
   return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries &&
+         g.K <= 32;
+}
+
+// fused tcgen05 dq: coarse chunks of <= 4 entries, K <= 32 fine blocks per row
+bool dqf_path(const Geometry& g) {
+  const char* e = getenv("LLSA_NO_TCGEN05");
+  const char* f = getenv("LLSA_DQF");
+  const uint32_t nce = coarse_entries(g);
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= dqf::kMaxEntries &&
          g.K <= 32;
 }
 
@@ -2507,6 +2932,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dqf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dqf::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_pipe_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, dqp::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_coarse_kernel,
@@ -2522,16 +2949,29 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                                        KvCfg<false>::Smem));
     attr = true;
   }
+  const bool dqf = dqf_path(g);
+  if (dqf) {
+    TmaMaps maps{};
+    const uint64_t in_rows = (uint64_t)units * g.n;
+    if (llsa_status st = make_tma_map(&maps.q, q, in_rows, kTileQ)) return st;
+    if (llsa_status st = make_tma_map(&maps.g, d_out, in_rows, kTileQ)) return st;
+    const uint64_t tiles = (g.n / kTileQ) * units;
+    const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
+    tc5_dqf_kernel<<<grid, dqf::kThreads, dqf::kSmem, s>>>(P, maps, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc5_dqf_kernel");
+    LLSA_MARK(mk, "bwd_dq", s);
+  }
   // dq: fine part (+ D, lse2) on mma.sync; coarse part on tcgen05 when enabled
-  const bool dq5 = P.nce > 0 && rows_path(g);
-  {
+  const bool dq5 = !dqf && P.nce > 0 && rows_path(g);
+  if (!dqf) {
     TcParams Pf = P;
     if (dq5) Pf.nce = 0;
     tc_dq_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kDqSmem, s>>>(Pf);
     count_launch();
     LLSA_LAUNCH_CHECK("tc_dq_kernel");
   }
-  LLSA_MARK(mk, "bwd_dq", s);
+  if (!dqf) LLSA_MARK(mk, "bwd_dq", s);
   if (dq5) {
     const char* old = getenv("LLSA_DQ5_SYNC");
     if (old && old[0] == '1') {
@@ -2554,7 +2994,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       LLSA_LAUNCH_CHECK("tc5_dq_pipe_kernel");
     }
   }
-  LLSA_MARK(mk, "bwd_dq_coarse_tc5", s);
+  if (dq5) LLSA_MARK(mk, "bwd_dq_coarse_tc5", s);
   // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
   const uint32_t start = P.rows_on ? P.rl_count : 0;
   if (P.rows_on) {

@@ -13,6 +13,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <cstdio>
 
 namespace llsa_umma {
 
@@ -76,6 +77,25 @@ __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
+#ifdef LLSA_HANG_DEBUG
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (it == (1ll << 22)) {
+      printf("HANG block %d thread %d mbar smem+0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             mbar, phase);
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -85,6 +105,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
       "r"(phase), "r"(0x989680)  // suspend-time hint (ns): sleep instead of spinning
       : "memory");
 }
+#endif
 
 __device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");

@@ -16,17 +16,23 @@ h = llsa.LLSAHandle(llsa.LLSAConfig(n, 64, 16, 8, 3, 3), units)
 out = torch.empty(units, n, 64, device="cuda")
 lib = llsa._lib.load()
 buf = (C.c_ulonglong * 8192)()
+which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
+dO = torch.randn_like(q)
+g = [torch.empty(units, n, 64, device="cuda") for _ in range(3)]
 for it in range(2):
-    lib.llsa_debug_trace(buf, 8192)  # reset
     h.forward(q, k, v, out)
     torch.cuda.synchronize()
+    lib.llsa_debug_trace(buf, 8192)  # reset
+    if which == "bwd":
+        h.backward(dO, q, k, v, out, *g)
+        torch.cuda.synchronize()
 cnt = lib.llsa_debug_trace(buf, 8192)
 ev = []
 for idx, x in enumerate(buf[:cnt]):
     if x >> 63:
         ev.append((idx // 1024, (idx // 32) % 32, idx % 32, x & 0x7FFFFFFFFFFFFFFF))
 t0 = min(e[3] for e in ev)
-names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"}
+names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "MMA", 4: "softmax"}
 ev.sort(key=lambda e: e[3])
 for r, t, e, c in ev:
     if t < 8:
