@@ -2270,7 +2270,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
   if (tid == 0) {
     mbar_init(bar(QFULL), 1);
-    mbar_init(bar(QEMPTY), 1 + 256);
+    mbar_init(bar(QEMPTY), 1);  // S/dP MMAs of the tile done
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(KFULL + i), 1);
       mbar_init(bar(KEMPTY + i), 1);
@@ -2530,7 +2530,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
         load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
       };
+      // this warp's own 16 Q and dO rows go to ring stage 1 (free until block 1)
       load_fine(0);
+      load_block16_async(sF + 4096, p.q + in_off + (q0 + fw * 16) * kD, bl, lane);
+      load_block16_async(sF + 4096 + kTile16, p.dout + in_off + (q0 + fw * 16) * kD, bl, lane);
       cp_async_commit();
       next_ids = fine_ids(id + gridDim.x);
       // D = rowsum(dO∘O) (fp32 O) and the log2 LSE of this warp's 16 rows;
@@ -2545,12 +2548,13 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         for (int k = 0; k < 8; ++k) ov[k] = o4[k];
       }
       const float lse_r = p.rm_in[ro + trow] * kLog2e + __log2f(p.rd_in[ro + trow]);
-      mbar_wait(bar(QFULL), i & 1);
+      cp_async_wait<0>();
+      __syncwarp();
       uint32_t qf[4][4], gf[4][4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        lda(sbase + kOffQ, fw * 16, ks, lane, qf[ks]);
-        lda(sbase + kOffG, fw * 16, ks, lane, gf[ks]);
+        lda(sF + 4096, 0, ks, lane, qf[ks]);
+        lda(sF + 4096 + kTile16, 0, ks, lane, gf[ks]);
       }
       float dsum = 0.f;
 #pragma unroll
@@ -2558,7 +2562,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         uint4 gv;
         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n"
                      : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
-                     : "r"(sbase + kOffG + swz(fw * 16 + rr, half * 4 + k)));
+                     : "r"(sF + 4096 + kTile16 + swz(rr, half * 4 + k)));
         const uint32_t w[4] = {gv.x, gv.y, gv.z, gv.w};
         const float of[8] = {ov[2 * k].x, ov[2 * k].y, ov[2 * k].z, ov[2 * k].w,
                              ov[2 * k + 1].x, ov[2 * k + 1].y, ov[2 * k + 1].z, ov[2 * k + 1].w};
@@ -2568,7 +2572,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           dsum = fmaf(__uint_as_float(w[t] & 0xffff0000u), of[2 * t + 1], dsum);
         }
       }
-      mbar_arrive(bar(QEMPTY));
+      __syncwarp();  // stage 1 is overwritten by fine block 1
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
       const uint32_t tb = i & 1;
       if (half == 0) {
