@@ -2617,6 +2617,349 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// backward: fine dK/dV on tcgen05 — persistent, key-major, warp-specialised
+// ---------------------------------------------------------------------------
+// Work item = one fine key block kb (16 keys) of one unit; its queries are the
+// CSC segment of kb (query blocks that selected it), gathered 8 blocks (128
+// queries) per chunk.  Per chunk:
+//   S  = Q_g K_kb^T, dP = dO_g V_kb^T      M = 128 gathered queries, N = 16
+//   thread = query: dS = P∘(dP − D), P = exp2(S c + b − lse)
+//   B' = [dS | P | 0] (bf16, MN-major [query][64]) → smem
+//   Acc += [Q_g^T ; dO_g^T] · B'           M = 128 (d of Q, d of dO), N = 64,
+//                                          K = the chunk's valid queries
+// so Acc[0:64, 0:16] = dK^T and Acc[64:128, 16:32] = dV^T accumulate in TMEM
+// over the item's chunks (no atomics).  The epilogue adds every coarse level's
+// pooled adjoint (already reduced) and writes dk, dv once.
+// Replaces P/src/attention_grad.cpp:43-73,127-135 (+ :149-161,184-196).
+//   warps 0,2,11,12  cp.async gather (Q, dO rows of the segment; K, V of kb;
+//                    lse, D) → 4-stage ring, completion via
+//                    cp.async.mbarrier.arrive; chunk facts in smem
+//   warp 1 (1 ln)    S / dP issuer;  warp 13 (1 ln)  accumulate issuer
+//   warps 3-6        softmax, thread = gathered query (TMEM lane)
+//   warps 7-10       epilogue, thread = head-dim row of Acc (TMEM lane)
+// Item facts (CSC offsets, query-block ids, coarse adjoint rows) are fetched
+// two items ahead so no dependent global load sits on a role's critical path.
+namespace kvf {
+constexpr int kQOff = 0, kGOff = 16384, kKOff = 32768, kVOff = 34816, kLseOff = 36864,
+              kDOff = 37376;
+constexpr int kStage = 38912;                  // 38 KB, 1024-aligned
+constexpr int kRing = 4;
+constexpr int kOffB = kRing * kStage;          // 152 KB: B' x 2 (16 KB each)
+constexpr int kOffInfo = kOffB + 2 * 16384;    // per-stage chunk facts
+constexpr int kOffBar = kOffInfo + 64;
+enum { FULL = 0, EMPTY = 4, SREADY = 8, SFREE = 10, BREADY = 12, BFREE = 14, AREADY = 16,
+       AFREE = 18, NBAR = 20 };
+constexpr int kSmem = kOffBar + NBAR * 8 + 16;
+constexpr int kThreads = 14 * 32;    // gather 0, 2, 11, 12; MMA 1, 13; softmax 3-6; epilogue 7-10
+constexpr uint32_t kTmemCols = 256;  // S|dP x 2 at [0, 64), Acc x 2 at 64, 128
+}  // namespace kvf
+
+__global__ void __launch_bounds__(kvf::kThreads, 1)
+    tc5_kvf_kernel(const __grid_constant__ TcParams p, uint32_t units) {
+  using namespace llsa_umma;
+  using namespace kvf;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
+  uint32_t* info = reinterpret_cast<uint32_t*>(smem + kOffInfo);  // [stage]: mc | first | last
+  const uint64_t nkb = p.n / kBS;
+  const uint64_t total = nkb * units;
+  // B' columns 32-63 stay zero for the whole kernel
+  for (uint32_t x = tid; x < 2 * 128 * 4; x += blockDim.x) {
+    const uint32_t b = x >> 9, r = (x >> 2) & 127, c = 4 + (x & 3);
+    *reinterpret_cast<uint4*>(smem + kOffB + b * 16384 + swz(r, c)) = make_uint4(0, 0, 0, 0);
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(bar(FULL + i), 128);  // every gather lane, via its copies
+      mbar_init(bar(EMPTY + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(SREADY + i), 1);
+      mbar_init(bar(SFREE + i), 128);
+      mbar_init(bar(BREADY + i), 128);
+      mbar_init(bar(BFREE + i), 1);
+      mbar_init(bar(AREADY + i), 1);
+      mbar_init(bar(AFREE + i), 128);
+    }
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  // CSC segment of item `id`: (first flat index, length)
+  auto segment = [&](uint64_t id, uint32_t& unit, uint64_t& kb, const uint32_t*& seg) {
+    unit = (uint32_t)(id / nkb);
+    kb = id % nkb;
+    const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[0];
+    seg = p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[0] + off[kb];
+    return off[kb + 1] - off[kb];
+  };
+
+  if (warp == 0 || warp == 2 || warp == 11 || warp == 12) {
+    // ------------------------------------------------------------ gather
+    // Four warps share every chunk (warp gi: query blocks gi and gi + 4;
+    // warp 0 also K_kb, V_kb, lse, D and the chunk facts).  Every lane's
+    // copies arrive on the chunk's FULL barrier asynchronously
+    // (cp.async.mbarrier.arrive.noinc, 128 arrivals), so the gather never
+    // blocks on its own copies; the MMA issuer fences the generic→async
+    // proxy after the wait.
+    const uint32_t gi = warp == 0 ? 0u : warp == 2 ? 1u : warp - 9;
+    const Block16Lane bl = block16_lane(lane);
+    const uint64_t nqb = p.n / kBS;
+    // Item facts are software-pipelined so no dependent global load sits on
+    // the issue path: the CSC offsets of item i+2 and the first 32 query-block
+    // ids of item i+1 are in flight while item i is issued.
+    const uint32_t* off0 = p.csc_off + p.csc_off_off[0];
+    const uint32_t* flat0 = p.csc_flat + p.csc_flat_off[0];
+    auto offs = [&](uint64_t id, uint32_t& lo, uint32_t& hi) {
+      lo = hi = 0;
+      if (id >= total) return;
+      const uint32_t* o = off0 + (id / nkb) * p.csc_off_entries + id % nkb;
+      lo = o[0];
+      hi = o[1];
+    };
+    auto ids = [&](uint64_t id, uint32_t lo, uint32_t hi) -> uint32_t {
+      return id < total && lo + lane < hi ? flat0[(id / nkb) * p.csc_flat_entries + lo + lane]
+                                          : 0u;
+    };
+    const uint64_t G = gridDim.x;
+    uint32_t lo0, hi0, lo1, hi1, lo2, hi2;
+    offs(blockIdx.x, lo0, hi0);
+    offs(blockIdx.x + G, lo1, hi1);
+    uint32_t ids0 = ids(blockIdx.x, lo0, hi0);
+    uint32_t ids1 = ids(blockIdx.x + G, lo1, hi1);
+    uint32_t rc = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += G) {
+      offs(id + 2 * G, lo2, hi2);
+      const uint32_t unit = (uint32_t)(id / nkb);
+      const uint64_t kb = id % nkb;
+      const uint32_t m = hi0 - lo0;
+      const uint32_t* seg = flat0 + (uint64_t)unit * p.csc_flat_entries + lo0;
+      const uint64_t in_off = (uint64_t)unit * p.n * kD, ro = (uint64_t)unit * p.n;
+      const uint32_t nch = (m + 7) / 8;
+      for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
+        const uint32_t s = rc % kRing;
+        const uint32_t mc = min(8u, m - ch * 8);
+        if (rc >= (uint32_t)kRing) mbar_wait(bar(EMPTY + s), ((rc / kRing) - 1) & 1);
+        const uint32_t st = sbase + s * kStage;
+        const uint32_t jj = ch * 8 + lane;
+        const uint32_t pre = __shfl_sync(0xffffffffu, ids0, jj & 31);
+        uint32_t qb = lane >= mc ? 0u : jj < 32 ? pre : seg[jj];
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+          const uint32_t b = gi + 4 * h;
+          const uint64_t t0 = (uint64_t)__shfl_sync(0xffffffffu, qb, b) * kBS;
+          if (b < mc) {
+            load_block16_async(st + kQOff + b * 2048, p.q + in_off + t0 * kD, bl, lane);
+            load_block16_async(st + kGOff + b * 2048, p.dout + in_off + t0 * kD, bl, lane);
+          }
+        }
+        const uint64_t tl = (uint64_t)__shfl_sync(0xffffffffu, qb, lane >> 2) * kBS + (lane & 3) * 4;
+        if (gi == 0) {
+          load_block16_async(st + kKOff, p.k + in_off + kb * kBS * kD, bl, lane);
+          load_block16_async(st + kVOff, p.v + in_off + kb * kBS * kD, bl, lane);
+          if ((lane >> 2) < mc) {
+            cp_async16(st + kLseOff + lane * 16, p.lse2 + ro + tl);
+            cp_async16(st + kDOff + lane * 16, p.drow + ro + tl);
+          }
+          if (lane == 0)
+            info[s] = mc | (ch == 0 ? 0x100u : 0u) | (ch + 1 == nch ? 0x200u : 0u);
+        }
+        cp_async_mbar_arrive(bar(FULL + s));
+      }
+      lo0 = lo1;
+      hi0 = hi1;
+      ids0 = ids1;
+      lo1 = lo2;
+      hi1 = hi2;
+      ids1 = ids(id + 2 * G, lo1, hi1);
+    }
+    // terminal marker
+    {
+      const uint32_t s = rc % kRing;
+      if (rc >= (uint32_t)kRing) mbar_wait(bar(EMPTY + s), ((rc / kRing) - 1) & 1);
+      if (gi == 0 && lane == 0) info[s] = 0x400u;
+      __syncwarp();
+      mbar_arrive(bar(FULL + s));
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ S / dP issuer
+    if (lane == 0) {
+      const uint32_t idesc_s = idesc_bf16(128, 16, false, false);
+      for (uint32_t c = 0;; ++c) {
+        const uint32_t s = c % kRing, b = c & 1;
+        mbar_wait(bar(FULL + s), (c / kRing) & 1);
+        if (info[s] & 0x400u) break;
+        if (c >= 2) mbar_wait(bar(SFREE + b), ((c >> 1) - 1) & 1);
+        fence_proxy_async();  // the gather's cp.async writes → the MMA's async proxy
+        fence_after();
+        const uint32_t st = sbase + s * kStage;
+        const uint32_t tS = tmem + 32 * b, tP = tS + 16;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          mma_bf16(tS, desc_kmajor(st + kQOff + ks * kKStepKMajor),
+                   desc_kmajor(st + kKOff + ks * kKStepKMajor), idesc_s, ks > 0);
+          mma_bf16(tP, desc_kmajor(st + kGOff + ks * kKStepKMajor),
+                   desc_kmajor(st + kVOff + ks * kKStepKMajor), idesc_s, ks > 0);
+        }
+        commit(bar(SREADY + b));
+      }
+    }
+  } else if (warp == 13) {
+    // ------------------------------------------------------------ dK/dV issuer
+    // (a second MMA-issuing thread: the S/dP of chunk c+1 and the accumulate
+    // of chunk c are issued concurrently)
+    if (lane == 0) {
+      const uint32_t idesc_a = idesc_bf16(128, 64, true, true);
+      uint32_t ai = 0;
+      for (uint32_t c = 0;; ++c) {
+        const uint32_t s = c % kRing, b = c & 1;
+        mbar_wait(bar(FULL + s), (c / kRing) & 1);
+        const uint32_t inf = info[s];
+        if (inf & 0x400u) break;
+        const uint32_t mc = inf & 0xFF, first = (inf >> 8) & 1, last = (inf >> 9) & 1;
+        const uint32_t ab = ai & 1;
+        mbar_wait(bar(BREADY + b), (c >> 1) & 1);
+        if (first && ai >= 2) mbar_wait(bar(AFREE + ab), ((ai >> 1) - 1) & 1);
+        fence_proxy_async();
+        fence_after();
+        const uint32_t st = sbase + s * kStage;
+        const uint32_t sb = sbase + kOffB + b * 16384;
+        const uint32_t ta = tmem + 64 + 64 * ab;
+        for (uint32_t ks = 0; ks < mc; ++ks)  // 16 gathered queries per k-step
+          mma_bf16(ta, desc_mnmajor(st + kQOff + ks * kKStepMNMajor, kGOff - kQOff),
+                   desc_mnmajor(sb + ks * kKStepMNMajor, 8192), idesc_a,
+                   (first && ks == 0) ? 0u : 1u);
+        commit(bar(EMPTY + s));
+        commit(bar(BFREE + b));
+        if (last) {
+          commit(bar(AREADY + ab));
+          ++ai;
+        }
+      }
+    }
+  } else if (warp >= 3 && warp < 7) {
+    // ------------------------------------------------------------ softmax warps
+    const uint32_t row = 32 * (warp & 3) + lane;  // gathered query (TMEM lane)
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    const float c2 = p.scale * kLog2e, bias = p.bias2[0];
+    for (uint32_t c = 0;; ++c) {
+      {
+        const uint32_t s = c % kRing, b = c & 1;
+        mbar_wait(bar(FULL + s), (c / kRing) & 1);
+        if (info[s] & 0x400u) break;
+        if (tid == 96) trace_ev(p, 4, c, 0);
+        mbar_wait(bar(SREADY + b), (c >> 1) & 1);
+        fence_after();
+        if (tid == 96) trace_ev(p, 4, c, 2);
+        uint32_t sv[32];
+        tmem_ld32(tmem + lane_off + 32 * b, sv);  // S (16) | dP (16)
+        tmem_ld_wait();
+        fence_before();
+        mbar_arrive(bar(SFREE + b));
+        const uint32_t mc = info[s] & 0xFF;
+        const bool valid = row < 16 * mc;
+        const float* lse = reinterpret_cast<const float*>(smem + s * kStage + kLseOff);
+        const float* Dq = reinterpret_cast<const float*>(smem + s * kStage + kDOff);
+        const float nb = bias - (valid ? lse[row] : 0.f), Dr = valid ? Dq[row] : 0.f;
+        uint32_t ds[8], pp[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float p0 = ex2(fmaf(__uint_as_float(sv[2 * k]), c2, nb));
+          float p1 = ex2(fmaf(__uint_as_float(sv[2 * k + 1]), c2, nb));
+          float d0 = p0 * (__uint_as_float(sv[16 + 2 * k]) - Dr);
+          float d1 = p1 * (__uint_as_float(sv[16 + 2 * k + 1]) - Dr);
+          if (!valid) p0 = p1 = d0 = d1 = 0.f;
+          pp[k] = pack_bf16(p0, p1);
+          ds[k] = pack_bf16(d0, d1);
+        }
+        if (c >= 2) mbar_wait(bar(BFREE + b), ((c >> 1) - 1) & 1);
+        const uint32_t sb = sbase + kOffB + b * 16384;
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sb + swz(row, 0)),
+                     "r"(ds[0]), "r"(ds[1]), "r"(ds[2]), "r"(ds[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sb + swz(row, 1)),
+                     "r"(ds[4]), "r"(ds[5]), "r"(ds[6]), "r"(ds[7]));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sb + swz(row, 2)),
+                     "r"(pp[0]), "r"(pp[1]), "r"(pp[2]), "r"(pp[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sb + swz(row, 3)),
+                     "r"(pp[4]), "r"(pp[5]), "r"(pp[6]), "r"(pp[7]));
+        fence_proxy_async();
+        mbar_arrive(bar(BREADY + b));
+        if (tid == 96) trace_ev(p, 4, c, 1);
+      }
+    }
+  } else if (warp >= 7) {
+    // ------------------------------------------------------------ epilogue warps
+    const uint32_t qd = warp & 3;                  // TMEM lane quadrant
+    const bool is_v = qd >= 2;                     // rows 64-127: dO^T → dV
+    const uint32_t dcol = lane + 32 * (qd & 1);    // head-dim column
+    const uint32_t lane_off = (32u * qd) << 16;
+    // per item: segment length and the sum of the coarse pooled-adjoint rows
+    // for this column (B = 16 here: level-l row of token t is t >> 4l),
+    // fetched two items ahead
+    auto facts = [&](uint64_t id, uint32_t& m, float& add) {
+      m = 0;
+      add = 0.f;
+      if (id >= total) return;
+      const uint32_t unit = (uint32_t)(id / nkb);
+      const uint64_t kb = id % nkb;
+      const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[0];
+      m = off[kb + 1] - off[kb];
+      for (uint32_t sl = 0; sl < p.ncl; ++sl) {
+        const uint32_t l = p.cl_level[sl];
+        const float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
+        const float* src = is_v ? gk + (uint64_t)p.cl_split[sl] * (p.n >> (4 * l)) * kD : gk;
+        add += src[((kb * kBS) >> (4 * l)) * kD + dcol];
+      }
+    };
+    uint32_t ai = 0, m1, m2;
+    float add1, add2;
+    facts(blockIdx.x, m1, add1);
+    facts(blockIdx.x + gridDim.x, m2, add2);
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x) {
+      const uint32_t m = m1;
+      const float add = add1;
+      m1 = m2;
+      add1 = add2;
+      facts(id + 2 * gridDim.x, m2, add2);
+      const uint32_t unit = (uint32_t)(id / nkb);
+      const uint64_t kb = id % nkb;
+      float acc[16];
+      if (m) {
+        const uint32_t ab = ai & 1;
+        if (tid == 224) trace_ev(p, 5, ai, 0);
+        mbar_wait(bar(AREADY + ab), (ai >> 1) & 1);
+        if (tid == 224) trace_ev(p, 5, ai, 1);
+        fence_after();
+        uint32_t r[16];
+        tmem_ld16(tmem + lane_off + 64 + 64 * ab + (is_v ? 16 : 0), r);
+        tmem_ld_wait();
+        fence_before();
+        mbar_arrive(bar(AFREE + ab));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(r[j]) * (is_v ? 1.f : p.scale);
+        ++ai;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      }
+      float* dst = (is_v ? p.dv : p.dk) + ((uint64_t)unit * p.n + kb * kBS) * kD + dcol;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -2663,6 +3006,13 @@ bool fwd5_path(const Geometry& g) {
   const uint32_t nce = coarse_entries(g);
   return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries &&
          g.K <= 32;
+}
+
+// tcgen05 fine dK/dV (key-major, gathered queries as M)
+bool kvf_path(const Geometry& g) {
+  const char* e = getenv("LLSA_NO_TCGEN05");
+  const char* f = getenv("LLSA_KVF");
+  return !(e && e[0] == '1') && !(f && f[0] == '0');
 }
 
 // fused tcgen05 dq: coarse chunks of <= 4 entries, K <= 32 fine blocks per row
@@ -2936,6 +3286,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kvf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kvf::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dqf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        dqf::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dq_pipe_kernel,
@@ -3046,7 +3398,13 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_LAUNCH_CHECK("reduce_parts_kernel");
   }
   LLSA_MARK(mk, "bwd_kv_coarse", s);
-  {
+  if (kvf_path(g)) {
+    const uint64_t items = (g.n / kBS) * units;
+    const unsigned grid = (unsigned)(items < (uint64_t)num_sms() ? items : num_sms());
+    tc5_kvf_kernel<<<grid, kvf::kThreads, kvf::kSmem, s>>>(P, units);
+    count_launch();
+    LLSA_LAUNCH_CHECK("tc5_kvf_kernel");
+  } else {
     const uint64_t tasks = g.n / kBS;
     const uint64_t warps = tasks * units;
     tc_kv_kernel<0><<<(unsigned)((warps + kKvWarps - 1) / kKvWarps), kKvWarps * 32,
