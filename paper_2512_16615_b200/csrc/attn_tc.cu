@@ -1772,7 +1772,8 @@ enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 8, VFULL = 12, VEMPTY = 15, SR
        SFREE = 24, PFULL = 30, PEMPTY = 32, OREADY = 34, OFREE = 36, FDONE = 38, FFREE = 39,
        NBAR = 40 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
-constexpr int kThreads = 16 * 32;  // 0 K' gather, 1 MMA, 2 V' gather, 3-6 coarse, 7-14 fine, 15 Q TMA
+constexpr int kThreads = 16 * 32;  // 0 K' gather, 1 S MMA, 2 V' gather, 3-6 coarse, 7-14 fine,
+                                   // 15 Q TMA + PV MMA
 constexpr uint32_t kTmemCols = 512;  // S: [0, 384), O: 384 + 64·buffer
 constexpr uint32_t kMaxEntries = 4 * kMaxChunks;
 }  // namespace fw5
@@ -1905,32 +1906,14 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       __syncwarp();
       if (lane == 0 && prev_full) mbar_arrive(prev_full);
     }
-  } else if (warp == 15) {
-    // ------------------------------------------------------------ Q producer
-    // Q(i+1) is issued as soon as tile i's S MMAs and fine warps release the
-    // buffer, independent of the coarse K'/V' rings.
-    if (lane == 0) {
-      prefetch_map(&m.q);
-      uint32_t i = 0;
-      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-        const uint32_t unit = (uint32_t)(id / tpu);
-        const uint64_t q0 = (id % tpu) * kTileQ;
-        const uint32_t qs = i % kQStages;
-        if (i >= (uint32_t)kQStages) mbar_wait(bar(QEMPTY + qs), ((i / kQStages) - 1) & 1);
-        mbar_expect_tx(bar(QFULL + qs), kQBytes);
-        tma_load_2d(sbase + kOffQ + qs * kQBytes, &m.q, 0, (int)(unit * p.n + q0),
-                    bar(QFULL + qs));
-      }
-    }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // S chunk c of tile i reuses TMEM columns [64c, 64c+64) as soon as the
     // coarse warps have read chunk c of tile i-1 (per-chunk SREADY / SFREE).
     if (lane == 0) {
-      const uint32_t idesc_o = idesc_bf16(128, kD + 16, false, true);  // O | l_c
-      uint32_t kc = 0, vc = 0, pc = 0, i = 0;
+      uint32_t kc = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-        const uint32_t qs = i % kQStages, ob = i % nob;
+        const uint32_t qs = i % kQStages;
         mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
         const uint32_t sq = sbase + kOffQ + qs * kQBytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++kc) {
@@ -1954,6 +1937,31 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           trace_ev(p, 3, i, ch);
         }
         commit(bar(QEMPTY + qs));
+      }
+    }
+  } else if (warp == 15) {
+    // ------------------------------------------------------------ Q TMA + PV issuer
+    // A second MMA-issuing thread, so the S chunks of tile i+1 do not wait
+    // behind tile i's PV chunks.  It also streams the Q tiles: Q(i+1) goes
+    // into the (single) Q buffer once tile i's S MMAs are done, which tile
+    // i's PV needs anyway.
+    if (lane == 0) {
+      static_assert(kQStages == 1, "the Q schedule below assumes one Q buffer");
+      prefetch_map(&m.q);
+      auto load_q = [&](uint64_t id) {
+        mbar_expect_tx(bar(QFULL), kQBytes);
+        tma_load_2d(sbase + kOffQ, &m.q, 0, (int)((id / tpu) * p.n + (id % tpu) * kTileQ),
+                    bar(QFULL));
+      };
+      if (blockIdx.x < total) load_q(blockIdx.x);
+      const uint32_t idesc_o = idesc_bf16(128, kD + 16, false, true);  // O | l_c
+      uint32_t vc = 0, pc = 0, i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t ob = i % nob;
+        if (id + gridDim.x < total) {
+          mbar_wait(bar(QEMPTY), i & 1);  // S MMAs of tile i done, fine warps hold Q
+          load_q(id + gridDim.x);
+        }
         if (i >= nob) mbar_wait(bar(OFREE + ob), ((i / nob) - 1) & 1);
         const uint32_t tO = tmem + o_base + o_stride * ob;
         for (uint32_t ch = 0; ch < nch; ++ch, ++vc, ++pc) {
