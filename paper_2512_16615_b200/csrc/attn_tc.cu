@@ -2371,29 +2371,8 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       __syncwarp();  // ent_rows is rewritten for the next tile
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ S / dP issuer
     if (lane == 0) {
-      const uint32_t idesc_q = idesc_bf16(128, kD, false, true);
-      struct Prev {
-        uint32_t c, s, ne, first, last, ti;
-      } pv{};
-      bool have = false;
-      auto do_dq = [&](const Prev& x) {
-        const uint32_t b = x.c & 1, tb = x.ti & 1;
-        mbar_wait(bar(DSREADY + b), (x.c >> 1) & 1);
-        if (x.first && x.ti >= 2) mbar_wait(bar(DQFREE + tb), ((x.ti >> 1) - 1) & 1);
-        fence_after();
-        const uint32_t sds = sbase + kOffDS + b * kDSBytes;
-        const uint32_t khi = sbase + kOffC + x.s * kCStage;
-        const uint32_t tq = tmem + 256 + tb * 64;
-        for (uint32_t ks = 0; ks < x.ne; ++ks)
-          mma_bf16(tq, desc_kmajor(sds + ks * kKStepKMajor),
-                   desc_mnmajor(khi + ks * kKStepMNMajor, 8192), idesc_q,
-                   (x.first && ks == 0) ? 0u : 1u);
-        commit(bar(KEMPTY + x.s));
-        commit(bar(DSFREE + b));
-        if (x.last) commit(bar(DQREADY + tb));
-      };
       uint32_t c = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
         mbar_wait(bar(QFULL), i & 1);
@@ -2421,12 +2400,34 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           }
           commit(bar(SREADY + b));
           if (ch + 1 == nch) commit(bar(QEMPTY));
-          if (have) do_dq(pv);
-          pv = Prev{c, s, ne, ch == 0 ? 1u : 0u, ch + 1 == nch ? 1u : 0u, i};
-          have = true;
         }
       }
-      if (have) do_dq(pv);
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ dQ issuer
+    // (a second MMA-issuing thread: dQ of chunk c overlaps S/dP of chunk c+1)
+    if (lane == 0) {
+      const uint32_t idesc_q = idesc_bf16(128, kD, false, true);
+      uint32_t c = 0, i = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+        const uint32_t tb = i & 1;
+        for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
+          const uint32_t s = c % kCRing, b = c & 1, ne = ch_info[ch] & 0xFF;
+          mbar_wait(bar(DSREADY + b), (c >> 1) & 1);
+          if (ch == 0 && i >= 2) mbar_wait(bar(DQFREE + tb), ((i >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t sds = sbase + kOffDS + b * kDSBytes;
+          const uint32_t khi = sbase + kOffC + s * kCStage;
+          const uint32_t tq = tmem + 256 + tb * 64;
+          for (uint32_t ks = 0; ks < ne; ++ks)
+            mma_bf16(tq, desc_kmajor(sds + ks * kKStepKMajor),
+                     desc_mnmajor(khi + ks * kKStepMNMajor, 8192), idesc_q,
+                     (ch == 0 && ks == 0) ? 0u : 1u);
+          commit(bar(KEMPTY + s));
+          commit(bar(DSFREE + b));
+          if (ch + 1 == nch) commit(bar(DQREADY + tb));
+        }
+      }
     }
   } else if (warp >= 3 && warp < 7) {
     // ------------------------------------------------------------ coarse warps
