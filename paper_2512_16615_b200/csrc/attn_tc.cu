@@ -2280,7 +2280,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
     mbar_init(bar(QFULL), 1);
     mbar_init(bar(QEMPTY), 1);  // S/dP MMAs of the tile done
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(KFULL + i), 1);
+      mbar_init(bar(KFULL + i), 32);  // every gather lane, via its copies
       mbar_init(bar(KEMPTY + i), 1);
       mbar_init(bar(SREADY + i), 1);
       mbar_init(bar(TFREE + i), 128);
@@ -2317,37 +2317,31 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
     }
   } else if (warp == 0) {
     // ------------------------------------------------------------ K'/V' gather
+    // Lane e holds coarse entry e's pyramid row, resolved one tile ahead.
+    // Copies complete on KFULL asynchronously (cp.async.mbarrier.arrive, one
+    // arrival per lane); the S/dP issuer fences the proxy after its wait.
     const Block16Lane bl = block16_lane(lane);
+    auto entry_row = [&](uint64_t id) -> uint32_t {
+      if (id >= total || lane >= nce) return 0u;
+      const uint32_t unit = (uint32_t)(id / tpu);
+      uint32_t l, r;
+      coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, (id % tpu) * kTileQ / kBS,
+                   lane, l, r);
+      return (uint32_t)(unit * p.pyr_rows) + r;
+    };
+    uint32_t rows_next = entry_row(blockIdx.x);
     uint32_t rc = 0;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x) {
-      const uint32_t unit = (uint32_t)(id / tpu);
-      const uint64_t q0 = (id % tpu) * kTileQ;
-      if (lane < nce) {
-        uint32_t l, r;
-        coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, q0 / kBS, lane, l, r);
-        ent_rows[lane] = (uint32_t)(unit * p.pyr_rows) + r;
-      }
-      __syncwarp();
-      uint32_t prev_full = 0;
+      const uint32_t myrow = rows_next;
+      rows_next = entry_row(id + gridDim.x);
       for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
         const uint32_t s = rc % kCRing;
         const uint32_t info = ch_info[ch], ne = info & 0xFF;
         const bool lo = info & 0x100u;
-        if (rc >= (uint32_t)kCRing) {
-          // the slot is released by the dQ MMA two chunks back, which needs the
-          // previous chunk's S/dP first: publish that chunk before blocking
-          if (prev_full) {
-            cp_async_wait<0>();
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(prev_full);
-            prev_full = 0;
-          }
-          mbar_wait(bar(KEMPTY + s), ((rc / kCRing) - 1) & 1);
-        }
+        if (rc >= (uint32_t)kCRing) mbar_wait(bar(KEMPTY + s), ((rc / kCRing) - 1) & 1);
         const uint32_t dst = sbase + kOffC + s * kCStage;
         for (uint32_t e = 0; e < ne; ++e) {
-          const uint64_t o = (uint64_t)ent_rows[ch * 4 + e] * kD;
+          const uint64_t o = (uint64_t)__shfl_sync(0xffffffffu, myrow, ch * 4 + e) * kD;
           load_block16_async(dst + e * 2048, p.khi + o, bl, lane);
           load_block16_async(dst + 16384 + e * 2048, p.vhi + o, bl, lane);
           if (lo) {
@@ -2355,20 +2349,8 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             load_block16_async(dst + 24576 + e * 2048, p.vlo + o, bl, lane);
           }
         }
-        cp_async_commit();
-        if (prev_full) {
-          cp_async_wait<1>();
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(prev_full);
-        }
-        prev_full = bar(KFULL + s);
+        cp_async_mbar_arrive(bar(KFULL + s));
       }
-      cp_async_wait<0>();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0 && prev_full) mbar_arrive(prev_full);
-      __syncwarp();  // ent_rows is rewritten for the next tile
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ S / dP issuer
@@ -2381,6 +2363,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           const uint32_t s = c % kCRing, b = c & 1;
           mbar_wait(bar(KFULL + s), (c / kCRing) & 1);
           if (c >= 2) mbar_wait(bar(TFREE + b), ((c >> 1) - 1) & 1);
+          fence_proxy_async();  // gathered cp.async data → async proxy
           fence_after();
           const uint32_t info = ch_info[ch], ne = info & 0xFF;
           const bool lo = info & 0x100u;
@@ -2415,6 +2398,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           const uint32_t s = c % kCRing, b = c & 1, ne = ch_info[ch] & 0xFF;
           mbar_wait(bar(DSREADY + b), (c >> 1) & 1);
           if (ch == 0 && i >= 2) mbar_wait(bar(DQFREE + tb), ((i >> 1) - 1) & 1);
+          fence_proxy_async();
           fence_after();
           const uint32_t sds = sbase + kOffDS + b * kDSBytes;
           const uint32_t khi = sbase + kOffC + s * kCStage;
