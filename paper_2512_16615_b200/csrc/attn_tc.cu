@@ -3182,9 +3182,11 @@ static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* p
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,
-                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk) {
-  if (llsa_status st = launch_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
-  LLSA_MARK(mk, "fwd_prep", s);
+                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk, bool prepped) {
+  if (!prepped) {
+    if (llsa_status st = launch_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
+    LLSA_MARK(mk, "fwd_prep", s);
+  }
   TcParams P = make_params(g);
   P.q = static_cast<const bf16*>(q);
   P.k = static_cast<const bf16*>(k);

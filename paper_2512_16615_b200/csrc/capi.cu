@@ -726,16 +726,24 @@ llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, con
   take_launch_count();
   EventMarker* mk = h->timers[0];
   if (mk) mk->start(s);
-  llsa_status st = pyramid(g, h->units, q, h->dt, h->pyr_q, s);
-  if (!st) st = pyramid(g, h->units, k, h->dt, h->pyr_k, s);
-  if (!st) st = pyramid(g, h->units, v, h->dt, h->pyr_v, s);
+  llsa_status st = LLSA_OK;
+  const bool fused = fused_pyramid_ok(g);
+  if (fused) {  // one pass over q, k, v; emits the tensor-core hi/lo copies too
+    st = fused_pyramids(g, h->units, q, k, v, h->dt, h->pyr_q, h->pyr_k, h->pyr_v,
+                        h->tc ? h->tcb.k_hi : nullptr, h->tc ? h->tcb.k_lo : nullptr,
+                        h->tc ? h->tcb.v_hi : nullptr, h->tc ? h->tcb.v_lo : nullptr, s);
+  } else {
+    st = pyramid(g, h->units, q, h->dt, h->pyr_q, s);
+    if (!st) st = pyramid(g, h->units, k, h->dt, h->pyr_k, s);
+    if (!st) st = pyramid(g, h->units, v, h->dt, h->pyr_v, s);
+  }
   LLSA_MARK(mk, "compress", s);
   if (!st) st = hier_topk(g, h->units, h->pyr_q, h->pyr_k, h->tables, s);
   LLSA_MARK(mk, "select", s);
   if (!st) {
     if (h->tc) {
       st = tc_forward(g, h->units, q, k, v, h->pyr_k, h->pyr_v, h->tables, out, h->row_max,
-                      h->row_denom, h->tcb, s, mk);
+                      h->row_denom, h->tcb, s, mk, fused);
     } else {
       st = simt_forward(g, h->units, h->dt, q, k, v, h->pyr_k, h->pyr_v, h->tables, out,
                         h->row_max, h->row_denom, s);

@@ -9,6 +9,7 @@
 // + rows_out·d·4.
 #include "common.cuh"
 #include "internal.h"
+#include "tc.h"
 
 namespace llsa_impl {
 namespace {
@@ -153,6 +154,172 @@ llsa_status launch_pool_backward(const float* g, uint32_t units, uint64_t coarse
                                                           1.0f / (float)group, out, total);
   count_launch();
   LLSA_LAUNCH_CHECK("pool_backward_kernel");
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl
+
+// ---------------------------------------------------------------------------
+// Fused compression for the handle path (B = 16, d = 64): q, k and v in one
+// launch (blockIdx.y), levels 1 and 2 in the same CTA (level 2 pooled from
+// the CTA's own level-1 rows in shared memory, same sequential order, so
+// bit-identical to per-level pooling), levels >= 3 in a second small launch.
+// When `hilo` is given it also emits the tensor-core operand copies of the
+// key/value pyramids: gain_l·x split into bf16 hi + lo (SURVEY.md hard
+// part 3), which otherwise costs a separate pass over the pyramids.
+// ---------------------------------------------------------------------------
+namespace llsa_impl {
+namespace {
+
+struct PyrArgs {
+  const void* in[3];
+  float* out[3];
+  __nv_bfloat16* hi[3];   // [k, v] hi (index 1, 2), null for q or when unused
+  __nv_bfloat16* lo[3];
+  uint64_t n, pyr_rows, off[kMaxLevels + 2];
+  float gain[kMaxLevels + 2];
+  uint32_t units, L, bf16_in;
+};
+
+__device__ __forceinline__ void emit(const PyrArgs& a, int t, uint64_t idx, float v0, float v1,
+                                     float v2, float v3, float g) {
+  float4* o = reinterpret_cast<float4*>(a.out[t] + idx);
+  *o = make_float4(v0, v1, v2, v3);
+  if (a.hi[t]) {
+    const float x[4] = {v0 * g, v1 * g, v2 * g, v3 * g};
+    __nv_bfloat16 h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      h[i] = __float2bfloat16_rn(x[i]);
+      l[i] = __float2bfloat16_rn(x[i] - __bfloat162float(h[i]));
+    }
+    *reinterpret_cast<uint2*>(a.hi[t] + idx) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&h[0]) | 0u, *reinterpret_cast<uint32_t*>(&h[2]));
+    *reinterpret_cast<uint2*>(a.lo[t] + idx) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&l[0]), *reinterpret_cast<uint32_t*>(&l[2]));
+  }
+}
+
+// CTA = 512 input rows of one unit and tensor (32 level-1 rows, 2 level-2
+// rows); thread = (level-1 row, 4-column group).
+__global__ void __launch_bounds__(512) pyr12_kernel(PyrArgs a) {
+  __shared__ float l1[32][65];
+  const int t = blockIdx.y;
+  const uint64_t chunks = a.n / 512;
+  const uint64_t unit = blockIdx.x / chunks, c = blockIdx.x % chunks;
+  const uint32_t tid = threadIdx.x, r = tid >> 4, cg = tid & 15;
+  const uint64_t row0 = c * 512 + (uint64_t)r * 16;  // first input row of level-1 row
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (a.bf16_in) {
+    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(a.in[t]) +
+                               (unit * a.n + row0) * 64 + cg * 4;
+#pragma unroll 4
+    for (int b = 0; b < 16; ++b) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(src + b * 64));
+      acc[0] = __fadd_rn(acc[0], __uint_as_float(x.x << 16));
+      acc[1] = __fadd_rn(acc[1], __uint_as_float(x.x & 0xffff0000u));
+      acc[2] = __fadd_rn(acc[2], __uint_as_float(x.y << 16));
+      acc[3] = __fadd_rn(acc[3], __uint_as_float(x.y & 0xffff0000u));
+    }
+  } else {
+    const float* src = static_cast<const float*>(a.in[t]) + (unit * a.n + row0) * 64 + cg * 4;
+#pragma unroll 4
+    for (int b = 0; b < 16; ++b) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src + b * 64));
+      acc[0] = __fadd_rn(acc[0], x.x);
+      acc[1] = __fadd_rn(acc[1], x.y);
+      acc[2] = __fadd_rn(acc[2], x.z);
+      acc[3] = __fadd_rn(acc[3], x.w);
+    }
+  }
+  const float inv = 1.f / 16.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    acc[j] = __fmul_rn(acc[j], inv);
+    l1[r][cg * 4 + j] = acc[j];
+  }
+  const uint64_t pu = unit * a.pyr_rows;
+  emit(a, t, (pu + a.off[1] + c * 32 + r) * 64 + cg * 4, acc[0], acc[1], acc[2], acc[3],
+       a.gain[1]);
+  if (a.L < 2) return;
+  __syncthreads();
+  if (tid < 2 * 16) {  // level 2: rows 2c, 2c+1; thread = (row, column group)
+    const uint32_t r2 = tid >> 4, g2 = tid & 15;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < 16; ++b)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[j] = __fadd_rn(s[j], l1[r2 * 16 + b][g2 * 4 + j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s[j] = __fmul_rn(s[j], inv);
+    emit(a, t, (pu + a.off[2] + c * 2 + r2) * 64 + g2 * 4, s[0], s[1], s[2], s[3], a.gain[2]);
+  }
+}
+
+// levels >= 3 (tiny): thread = (unit, tensor, level row, 4-column group),
+// one level after another inside the CTA (each CTA owns one unit).
+__global__ void __launch_bounds__(256) pyr3_kernel(PyrArgs a) {
+  const int t = blockIdx.y;
+  const uint64_t unit = blockIdx.x;
+  const uint64_t pu = unit * a.pyr_rows;
+  const float inv = 1.f / 16.f;
+  for (uint32_t l = 3; l <= a.L; ++l) {
+    const uint64_t rows = a.n >> (4 * l);
+    for (uint64_t i = threadIdx.x; i < rows * 16; i += blockDim.x) {
+      const uint64_t r = i >> 4, g = i & 15;
+      const float* src = a.out[t] + (pu + a.off[l - 1] + r * 16) * 64 + g * 4;
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int b = 0; b < 16; ++b) {
+        const float4 x = *reinterpret_cast<const float4*>(src + b * 64);
+        s[0] = __fadd_rn(s[0], x.x);
+        s[1] = __fadd_rn(s[1], x.y);
+        s[2] = __fadd_rn(s[2], x.z);
+        s[3] = __fadd_rn(s[3], x.w);
+      }
+      emit(a, t, (pu + a.off[l] + r) * 64 + g * 4, __fmul_rn(s[0], inv), __fmul_rn(s[1], inv),
+           __fmul_rn(s[2], inv), __fmul_rn(s[3], inv), a.gain[l]);
+    }
+    __syncthreads();  // level l is complete before level l+1 reads it
+  }
+}
+
+}  // namespace
+
+bool fused_pyramid_ok(const Geometry& g) {
+  return g.B == 16 && g.d == 64 && g.n % 512 == 0 && g.L >= 1 && g.L <= kMaxLevels;
+}
+
+llsa_status fused_pyramids(const Geometry& g, uint32_t units, const void* q, const void* k,
+                           const void* v, llsa_dtype dt, float* pq, float* pk, float* pv,
+                           __nv_bfloat16* khi, __nv_bfloat16* klo, __nv_bfloat16* vhi,
+                           __nv_bfloat16* vlo, cudaStream_t s) {
+  PyrArgs a{};
+  a.in[0] = q;
+  a.in[1] = k;
+  a.in[2] = v;
+  a.out[0] = pq;
+  a.out[1] = pk;
+  a.out[2] = pv;
+  a.hi[1] = khi;
+  a.lo[1] = klo;
+  a.hi[2] = vhi;
+  a.lo[2] = vlo;
+  a.n = g.n;
+  a.pyr_rows = g.pyr_rows;
+  for (uint32_t l = 0; l <= g.L && l < kMaxLevels + 2; ++l) {
+    a.off[l] = g.pyr_off[l];
+    a.gain[l] = g.mode == 0 ? (float)g.pow[l] : 1.f;  // ScaleKV gain B^l, LogitBias 1
+  }
+  a.units = units;
+  a.L = g.L;
+  a.bf16_in = dt == LLSA_BF16 ? 1u : 0u;
+  pyr12_kernel<<<dim3((unsigned)(units * (g.n / 512)), 3), 512, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("pyr12_kernel");
+  if (g.L >= 3) {
+    pyr3_kernel<<<dim3(units, 3), 256, 0, s>>>(a);
+    count_launch();
+    LLSA_LAUNCH_CHECK("pyr3_kernel");
+  }
   return LLSA_OK;
 }
 

@@ -19,13 +19,23 @@ struct TcBuffers {
 };
 
 bool tc_supported(const Geometry& g, llsa_dtype dt);
+
+// Fused compression of q, k, v (pyramid.cu): B = 16, d = 64.  With non-null
+// hi/lo buffers it also writes the tensor-core key/value operand copies, so
+// tc_forward can skip its prep pass.
+bool fused_pyramid_ok(const Geometry& g);
+llsa_status fused_pyramids(const Geometry& g, uint32_t units, const void* q, const void* k,
+                           const void* v, llsa_dtype dt, float* pq, float* pk, float* pv,
+                           __nv_bfloat16* khi, __nv_bfloat16* klo, __nv_bfloat16* vhi,
+                           __nv_bfloat16* vlo, cudaStream_t s);
 size_t tc_buffer_bytes(const Geometry& g, uint32_t units);
 void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out);
 
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,
-                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk = nullptr);
+                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk = nullptr,
+                       bool prepped = false);
 size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units);
 llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                         const float* out, const float* row_max, const float* row_denom,
