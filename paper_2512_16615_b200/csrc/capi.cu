@@ -671,7 +671,8 @@ llsa_status llsa_handle_create(const llsa_config* cfg, uint32_t units, llsa_dtyp
   const size_t coff = al((size_t)units * g.csc_off_entries * 4);
   const size_t cflat = al((size_t)units * g.csc_flat_entries * 4);
   const size_t rows = al((size_t)units * g.n * 4);
-  h->tr_ws_bytes = al(transpose_all_ws(g, units));
+  h->tr_ws_bytes = al(transpose_all_fused_ok(g) ? transpose_all_fused_ws(g, units)
+                                                : transpose_all_ws(g, units));
   h->bwd_ws_bytes = al(h->tc ? tc_backward_ws_bytes(g, units) : simt_backward_ws_bytes(g, units));
   const size_t tcb = h->tc ? al(tc_buffer_bytes(g, units)) : 0;
   h->arena_bytes = 3 * pyr + tab + coff + cflat + 2 * rows + h->tr_ws_bytes + h->bwd_ws_bytes +
@@ -771,8 +772,11 @@ llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q
   take_launch_count();
   EventMarker* mk = h->timers[1];
   if (mk) mk->start(s);
-  llsa_status st = transpose_all_impl(g, h->units, h->tables, h->csc_off, h->csc_flat,
-                                      h->tr_ws, s);
+  llsa_status st = transpose_all_fused_ok(g)
+                        ? transpose_all_fused(g, h->units, h->tables, h->csc_off, h->csc_flat,
+                                              h->tr_ws, s)
+                        : transpose_all_impl(g, h->units, h->tables, h->csc_off, h->csc_flat,
+                                             h->tr_ws, s);
   LLSA_MARK(mk, "transpose", s);
   if (!st) {
     if (h->tc)

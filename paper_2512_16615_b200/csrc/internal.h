@@ -68,6 +68,11 @@ void count_launch(uint32_t n = 1);
 uint32_t take_launch_count();
 
 // ---- launchers (each returns LLSA_OK or an error; no synchronisation) ----
+// CSR → CSC of every selection level in four launches (transpose.cu)
+bool transpose_all_fused_ok(const Geometry& g);
+size_t transpose_all_fused_ws(const Geometry& g, uint32_t units);
+llsa_status transpose_all_fused(const Geometry& g, uint32_t units, const uint32_t* tables,
+                                uint32_t* offs, uint32_t* flat, void* ws, cudaStream_t s);
 llsa_status launch_pool_level(const void* in, llsa_dtype in_dtype, uint64_t in_unit_stride,
                               float* out, uint64_t out_unit_stride, uint32_t units,
                               uint64_t rows_out, uint32_t d, uint32_t B, cudaStream_t s);

@@ -167,3 +167,179 @@ llsa_status launch_transpose(const uint32_t* idx, uint64_t idx_unit_stride, uint
 }
 
 }  // namespace llsa_impl
+
+// ---------------------------------------------------------------------------
+// All levels at once (the handle path): the same four phases, one launch
+// each, blockIdx.y = level; per-level geometry in a by-value table.
+// ---------------------------------------------------------------------------
+namespace llsa_impl {
+namespace {
+
+constexpr int kTrMax = 8;
+struct TrAll {
+  const uint32_t* idx[kTrMax];
+  uint32_t* counts[kTrMax];
+  uint32_t* tmp[kTrMax];
+  uint32_t* offs[kTrMax];
+  uint32_t* flat[kTrMax];
+  uint32_t rows[kTrMax], kb[kTrMax];
+  uint64_t idx_stride, off_stride, flat_stride;
+  uint32_t units, k, levels;
+  uint32_t* flag;
+};
+
+__global__ void count_all_kernel(TrAll a) {
+  const uint32_t l = blockIdx.y;
+  const uint64_t per_unit = (uint64_t)a.rows[l] * a.k, total = per_unit * a.units;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e / per_unit, i = e - u * per_unit;
+    const uint32_t b = a.idx[l][u * a.idx_stride + i];
+    if (b >= a.kb[l]) {
+      raise_flag(a.flag, kErrIndex);
+      continue;
+    }
+    atomicAdd(&a.counts[l][u * a.kb[l] + b], 1u);
+  }
+}
+
+__global__ void __launch_bounds__(1024) scan_all_kernel(TrAll a) {
+  const uint32_t l = blockIdx.y;
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  const uint32_t u = blockIdx.x, kbn = a.kb[l];
+  uint32_t* cnt = a.counts[l] + (uint64_t)u * kbn;
+  uint32_t* off = a.offs[l] + (uint64_t)u * a.off_stride;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < kbn; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < kbn ? cnt[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= (uint32_t)o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - v;
+    if (i < kbn) {
+      off[i] = excl;
+      cnt[i] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[kbn] = carry;
+}
+
+__global__ void scatter_all_kernel(TrAll a) {
+  const uint32_t l = blockIdx.y;
+  const uint64_t per_unit = (uint64_t)a.rows[l] * a.k, total = per_unit * a.units;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e / per_unit, i = e - u * per_unit;
+    const uint32_t b = a.idx[l][u * a.idx_stride + i];
+    if (b >= a.kb[l]) continue;
+    const uint32_t pos = atomicAdd(&a.counts[l][u * a.kb[l] + b], 1u);
+    a.tmp[l][u * per_unit + pos] = (uint32_t)(i / a.k);
+  }
+}
+
+__global__ void segment_order_all_kernel(TrAll a) {
+  const uint32_t l = blockIdx.y;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp >= (uint64_t)a.kb[l] * a.units) return;
+  const uint64_t u = warp / a.kb[l], b = warp - u * a.kb[l];
+  const uint32_t* off = a.offs[l] + u * a.off_stride;
+  const uint32_t s0 = off[b], s1 = off[b + 1];
+  const uint32_t* seg = a.tmp[l] + u * (uint64_t)a.rows[l] * a.k + s0;
+  uint32_t* dst = a.flat[l] + u * a.flat_stride + s0;
+  const uint32_t len = s1 - s0;
+  for (uint32_t e = lane; e < len; e += 32) {
+    const uint32_t v = seg[e];
+    uint32_t rank = 0;
+    for (uint32_t e2 = 0; e2 < len; ++e2) {
+      const uint32_t w = seg[e2];
+      rank += (w < v || (w == v && e2 < e)) ? 1u : 0u;
+    }
+    dst[rank] = v;
+  }
+}
+
+}  // namespace
+
+bool transpose_all_fused_ok(const Geometry& g) { return g.L >= 1 && g.L <= kTrMax; }
+
+size_t transpose_all_fused_ws(const Geometry& g, uint32_t units) {
+  size_t b = 256;
+  for (uint32_t l = 0; l < g.L; ++l) {
+    b += ((size_t)units * g.level_blocks(l) * 4 + 255) & ~size_t(255);
+    b += ((size_t)units * g.level_blocks(l) * g.K * 4 + 255) & ~size_t(255);
+  }
+  return b;
+}
+
+llsa_status transpose_all_fused(const Geometry& g, uint32_t units, const uint32_t* tables,
+                                uint32_t* offs, uint32_t* flat, void* ws, cudaStream_t s) {
+  TrAll a{};
+  char* p = static_cast<char*>(ws);
+  size_t cbytes = 0;
+  uint64_t maxe = 0, maxkb = 0;
+  for (uint32_t l = 0; l < g.L; ++l) {  // counts of every level are contiguous (one memset)
+    a.counts[l] = reinterpret_cast<uint32_t*>(p + cbytes);
+    cbytes += ((size_t)units * g.level_blocks(l) * 4 + 255) & ~size_t(255);
+  }
+  size_t tb = cbytes;
+  for (uint32_t l = 0; l < g.L; ++l) {
+    const uint64_t rows = g.level_blocks(l), kb = g.level_blocks(l);  // square per level
+    a.tmp[l] = reinterpret_cast<uint32_t*>(p + tb);
+    tb += ((size_t)units * rows * g.K * 4 + 255) & ~size_t(255);
+    a.idx[l] = tables + g.table_off[l];
+    a.offs[l] = offs + g.csc_off_off[l];
+    a.flat[l] = flat + g.csc_flat_off[l];
+    a.rows[l] = (uint32_t)rows;
+    a.kb[l] = (uint32_t)kb;
+    maxe = rows * g.K > maxe ? rows * g.K : maxe;
+    maxkb = kb > maxkb ? kb : maxkb;
+  }
+  a.idx_stride = g.table_entries;
+  a.off_stride = g.csc_off_entries;
+  a.flat_stride = g.csc_flat_entries;
+  a.units = units;
+  a.k = g.K;
+  a.levels = g.L;
+  a.flag = device_flag();
+  LLSA_CUDA_TRY(cudaMemsetAsync(ws, 0, cbytes, s));
+  const dim3 ge(grid_for(maxe * units, 256), g.L);
+  count_all_kernel<<<ge, 256, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("count_all_kernel");
+  scan_all_kernel<<<dim3(units, g.L), 1024, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("scan_all_kernel");
+  scatter_all_kernel<<<ge, 256, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("scatter_all_kernel");
+  const uint64_t warps = maxkb * units;
+  segment_order_all_kernel<<<dim3((unsigned)((warps * 32 + 255) / 256), g.L), 256, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("segment_order_all_kernel");
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl
