@@ -2953,6 +2953,306 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
   if (warp == 0) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// backward: coarse dK'/dV' — persistent, warp-specialised tcgen05 version
+// ---------------------------------------------------------------------------
+// Same work items and partial layout as tc5_kv_rows_kernel (one item = level
+// l, selection row, query slice, group of 8 selected blocks = 128 keys as M),
+// but one CTA per SM walks the items and every stage overlaps the next:
+//   warp 15 (1 lane)   TMA: 64-query Q / dO tiles (2-D boxes) + lse, D (1-D
+//                      bulk) → 4-stage ring
+//   warp 0             cp.async gather of the item's key tiles (K', V' hi
+//                      [+ lo]) → completes via cp.async.mbarrier.arrive
+//   warp 1 (1 lane)    S^T = K' Q^T, dP^T = V' dO^T → TMEM (double buffer)
+//   warps 4-11         thread = key (TMEM lane) × 32 queries: P^T, dS^T → bf16
+//                      smem (double buffer)
+//   warp 2 (1 lane)    dV' += P^T dO, dK' += dS^T Q → TMEM (double buffer per
+//                      item)
+//   warps 3, 12-14     epilogue: the item's raw 128×64 dK', dV' partial → HBM
+// Replaces P/src/attention_grad.cpp:136-162 (levels 1..L-1).
+namespace rows2 {
+constexpr int kKeys = 128, kQT = 64;
+constexpr int kArr = kKeys * 128;                 // one 128-key array: 16 KB
+constexpr int kQStage = 17408;                    // Q 8 KB | dO 8 KB | lse | D, 1 KB aligned
+constexpr int kQRing = 4;
+template <bool LO>
+struct L {
+  static constexpr int kKeyBufs = LO ? 1 : 2;
+  static constexpr int kKeyBuf = (LO ? 4 : 2) * kArr;  // Khi, Vhi (, Klo, Vlo)
+  static constexpr int kOffQ = kKeyBufs * kKeyBuf;
+  static constexpr int kOffP = kOffQ + kQRing * kQStage;  // P^T, dS^T x 2
+  static constexpr int kOffBar = kOffP + 2 * 2 * 16384;
+  static constexpr int kSmem = kOffBar + 256;
+};
+enum { KFULL = 0, KEMPTY = 2, QFULL = 4, QEMPTY = 8, SREADY = 12, SFREE = 14, PREADY = 16,
+       PFREE = 18, AREADY = 20, AFREE = 22, NBAR = 24 };
+constexpr int kThreads = 16 * 32;
+constexpr uint32_t kTmemCols = 512;  // S^T|dP^T x 2 at [0, 256), dK'|dV' x 2 at [256, 512)
+}  // namespace rows2
+
+template <bool LO>
+__global__ void __launch_bounds__(rows2::kThreads, 1)
+    tc5_rows2_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TmaMaps m,
+                     uint32_t li, uint32_t units) {
+  using namespace llsa_umma;
+  using namespace rows2;
+  using Lay = L<LO>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  auto bar = [&](int i) { return sbase + Lay::kOffBar + 8u * i; };
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Lay::kOffBar + NBAR * 8);
+  const uint64_t tpu = p.rl_tasks[li + 1] - p.rl_tasks[li];
+  const uint64_t total = tpu * units;
+  const uint32_t level = p.rl_level[li], slices = p.rl_slices[li];
+  const uint64_t span = p.pow[level + 1], qs = p.rl_qs[li];
+  const uint32_t ntiles = (uint32_t)(qs / kQT);
+  const uint64_t G = gridDim.x;
+  // item → (unit, row, slice, group)
+  auto decode = [&](uint64_t id, uint32_t& unit, uint64_t& row, uint32_t& slice,
+                    uint32_t& group) {
+    unit = (uint32_t)(id / tpu);
+    const uint64_t task = id % tpu;
+    group = (uint32_t)(task % p.groups);
+    const uint64_t rs = task / p.groups;
+    slice = (uint32_t)(rs % slices);
+    row = rs / slices;
+  };
+  if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(KFULL + i), 32);  // every gather lane, via its copies
+      mbar_init(bar(KEMPTY + i), 1);
+      mbar_init(bar(SREADY + i), 1);
+      mbar_init(bar(SFREE + i), 256);
+      mbar_init(bar(PREADY + i), 256);
+      mbar_init(bar(PFREE + i), 1);
+      mbar_init(bar(AREADY + i), 1);
+      mbar_init(bar(AFREE + i), 128);
+    }
+    for (int i = 0; i < kQRing; ++i) {
+      mbar_init(bar(QFULL + i), 1);
+      mbar_init(bar(QEMPTY + i), 1);
+    }
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 15) {
+    // ------------------------------------------------------------ Q / dO TMA
+    if (lane == 0) {
+      prefetch_map(&m.q);
+      prefetch_map(&m.g);
+      uint32_t t = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += G) {
+        uint32_t unit, slice, group;
+        uint64_t row;
+        decode(id, unit, row, slice, group);
+        const uint64_t q_begin = row * span + (uint64_t)slice * qs;
+        const uint64_t ro = (uint64_t)unit * p.n;
+        for (uint32_t j = 0; j < ntiles; ++j, ++t) {
+          const uint32_t s = t % kQRing;
+          if (t >= (uint32_t)kQRing) mbar_wait(bar(QEMPTY + s), ((t / kQRing) - 1) & 1);
+          const uint32_t dst = sbase + Lay::kOffQ + s * kQStage;
+          const uint64_t t0 = q_begin + (uint64_t)j * kQT;
+          mbar_expect_tx(bar(QFULL + s), 2 * kQT * 128 + 2 * kQT * 4);
+          tma_load_2d(dst, &m.q, 0, (int)(ro + t0), bar(QFULL + s));
+          tma_load_2d(dst + kQT * 128, &m.g, 0, (int)(ro + t0), bar(QFULL + s));
+          bulk_load(dst + 2 * kQT * 128, p.lse2 + ro + t0, kQT * 4, bar(QFULL + s));
+          bulk_load(dst + 2 * kQT * 128 + kQT * 4, p.drow + ro + t0, kQT * 4, bar(QFULL + s));
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------------ key gather
+    const Block16Lane bl = block16_lane(lane);
+    const uint64_t nblk = p.n / p.pow[level + 1];
+    auto key_ids = [&](uint64_t id) -> uint32_t {  // lane < 8: the item's block id
+      if (id >= total || lane >= 8) return 0u;
+      uint32_t unit, slice, group;
+      uint64_t row;
+      decode(id, unit, row, slice, group);
+      uint32_t b = p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K +
+                            group * 8 + lane];
+      if (b >= nblk) {
+        raise_flag(p.flag, llsa_dev::kErrIndex);
+        b = 0;
+      }
+      return b;
+    };
+    uint32_t ids_next = key_ids(blockIdx.x);
+    uint32_t it = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+      const uint32_t ids = ids_next;
+      ids_next = key_ids(id + G);
+      const uint32_t kb = it % Lay::kKeyBufs;
+      if (it >= (uint32_t)Lay::kKeyBufs)
+        mbar_wait(bar(KEMPTY + kb), ((it / Lay::kKeyBufs) - 1) & 1);
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint32_t dst = sbase + kb * Lay::kKeyBuf;
+      const uint64_t base = (uint64_t)unit * p.pyr_rows + p.pyr_off[level];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint64_t o = (base + (uint64_t)__shfl_sync(0xffffffffu, ids, b) * kBS) * kD;
+        load_block16_async(dst + b * 2048, p.khi + o, bl, lane);
+        load_block16_async(dst + kArr + b * 2048, p.vhi + o, bl, lane);
+        if (LO) {
+          load_block16_async(dst + 2 * kArr + b * 2048, p.klo + o, bl, lane);
+          load_block16_async(dst + 3 * kArr + b * 2048, p.vlo + o, bl, lane);
+        }
+      }
+      cp_async_mbar_arrive(bar(KFULL + kb));
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ S^T / dP^T issuer
+    if (lane == 0) {
+      const uint32_t idesc_s = idesc_bf16(128, kQT, false, false);
+      uint32_t t = 0, it = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+        const uint32_t kb = it % Lay::kKeyBufs;
+        const uint32_t sK = sbase + kb * Lay::kKeyBuf;
+        for (uint32_t j = 0; j < ntiles; ++j, ++t) {
+          const uint32_t s = t % kQRing, b = t & 1;
+          if (j == 0) mbar_wait(bar(KFULL + kb), (it / Lay::kKeyBufs) & 1);
+          mbar_wait(bar(QFULL + s), (t / kQRing) & 1);
+          if (t >= 2) mbar_wait(bar(SFREE + b), ((t >> 1) - 1) & 1);
+          fence_proxy_async();  // gathered key tiles (cp.async) → async proxy
+          fence_after();
+          const uint32_t sQ = sbase + Lay::kOffQ + s * kQStage, sG = sQ + kQT * 128;
+          const uint32_t tS = tmem + 128 * b, tP = tS + 64;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bq = desc_kmajor(sQ + ks * kKStepKMajor);
+            const uint64_t bg = desc_kmajor(sG + ks * kKStepKMajor);
+            mma_bf16(tS, desc_kmajor(sK + ks * kKStepKMajor), bq, idesc_s, ks > 0);
+            mma_bf16(tP, desc_kmajor(sK + kArr + ks * kKStepKMajor), bg, idesc_s, ks > 0);
+            if (LO) {
+              mma_bf16(tS, desc_kmajor(sK + 2 * kArr + ks * kKStepKMajor), bq, idesc_s, 1);
+              mma_bf16(tP, desc_kmajor(sK + 3 * kArr + ks * kKStepKMajor), bg, idesc_s, 1);
+            }
+          }
+          commit(bar(SREADY + b));
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ dK'/dV' issuer
+    if (lane == 0) {
+      const uint32_t idesc_kv = idesc_bf16(128, kD, false, true);
+      uint32_t t = 0, it = 0;
+      for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+        const uint32_t kb = it % Lay::kKeyBufs, ab = it & 1;
+        const uint32_t tDK = tmem + 256 + 128 * ab, tDV = tDK + 64;
+        for (uint32_t j = 0; j < ntiles; ++j, ++t) {
+          const uint32_t s = t % kQRing, b = t & 1;
+          mbar_wait(bar(PREADY + b), (t >> 1) & 1);
+          if (j == 0 && it >= 2) mbar_wait(bar(AFREE + ab), ((it >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t sQ = sbase + Lay::kOffQ + s * kQStage, sG = sQ + kQT * 128;
+          const uint32_t sPT = sbase + Lay::kOffP + b * 32768, sDST = sPT + 16384;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {  // K = 64 queries
+            mma_bf16(tDV, desc_kmajor(sPT + ks * kKStepKMajor),
+                     desc_mnmajor(sG + ks * kKStepMNMajor, 8192), idesc_kv, (j | ks) > 0);
+            mma_bf16(tDK, desc_kmajor(sDST + ks * kKStepKMajor),
+                     desc_mnmajor(sQ + ks * kKStepMNMajor, 8192), idesc_kv, (j | ks) > 0);
+          }
+          commit(bar(QEMPTY + s));
+          commit(bar(PFREE + b));
+          if (j + 1 == ntiles) {
+            commit(bar(AREADY + ab));
+            commit(bar(KEMPTY + kb));
+          }
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------------------ softmax warps
+    const uint32_t krow = 32 * (warp & 3) + lane;   // key (TMEM lane)
+    const uint32_t qh = (warp - 4) >> 2;            // query columns [32 qh, +32)
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    const float c2 = p.scale * kLog2e, bias = p.bias2[level];
+    const uint32_t ntot = (uint32_t)((total + G - 1 - blockIdx.x) / G) * ntiles;
+    for (uint32_t t = 0; t < ntot; ++t) {
+      const uint32_t s = t % kQRing, b = t & 1;
+      mbar_wait(bar(QFULL + s), (t / kQRing) & 1);
+      mbar_wait(bar(SREADY + b), (t >> 1) & 1);
+      fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld32(tmem + lane_off + 128 * b + 32 * qh, sv);
+      tmem_ld32(tmem + lane_off + 128 * b + 64 + 32 * qh, pv);
+      tmem_ld_wait();
+      fence_before();
+      mbar_arrive(bar(SFREE + b));
+      const float* lse = reinterpret_cast<const float*>(smem + Lay::kOffQ + s * kQStage +
+                                                        2 * kQT * 128) + 32 * qh;
+      const float* Dq = lse + kQT;
+      if (t >= 2) mbar_wait(bar(PFREE + b), ((t >> 1) - 1) & 1);
+      const uint32_t sPT = sbase + Lay::kOffP + b * 32768, sDST = sPT + 16384;
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t pk[4], dk4[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float pe[2], de[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = c8 * 8 + h * 2 + e;
+            const float pr = ex2(fmaf(__uint_as_float(sv[i]), c2, bias - lse[i]));
+            pe[e] = pr;
+            de[e] = pr * (__uint_as_float(pv[i]) - Dq[i]);
+          }
+          pk[h] = pack_bf16(pe[0], pe[1]);
+          dk4[h] = pack_bf16(de[0], de[1]);
+        }
+        const uint32_t chunk = qh * 4 + c8;
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sPT + swz(krow, chunk)),
+                     "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sDST + swz(krow, chunk)),
+                     "r"(dk4[0]), "r"(dk4[1]), "r"(dk4[2]), "r"(dk4[3]));
+      }
+      fence_proxy_async();
+      mbar_arrive(bar(PREADY + b));
+    }
+  } else if (warp == 3 || warp >= 12) {
+    // ------------------------------------------------------------ epilogue warps
+    const uint32_t krow = 32 * (warp & 3) + lane;
+    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    uint32_t it = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+      uint32_t unit, slice, group;
+      uint64_t row;
+      decode(id, unit, row, slice, group);
+      const uint32_t ab = it & 1;
+      mbar_wait(bar(AREADY + ab), (it >> 1) & 1);
+      fence_after();
+      const uint64_t pidx = (row * slices + slice) * p.groups + group;
+      float* dst = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li] +
+                   pidx * (2 * kKeys * kD) + (uint64_t)krow * kD;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {  // dK' cols 0-63 then dV' (+64 in TMEM, +128 rows in HBM)
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + 256 + 128 * ab + 32 * q4, r);
+        tmem_ld_wait();
+        float* d = dst + (q4 >= 2 ? kKeys * kD : 0) + 32 * (q4 & 1);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(d + i) =
+              make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+      }
+      fence_before();
+      mbar_arrive(bar(AFREE + ab));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kTmemCols);
+}
+
 // split 0 of coarse slots [s0, s1) ← coefficient · Σ_splits (fixed order)
 __global__ void reduce_parts_kernel(TcParams p, uint32_t units, uint32_t s0, uint32_t s1) {
   for (uint32_t sl = s0; sl < s1; ++sl) {
@@ -3281,6 +3581,12 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<1>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<true>::Smem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_rows2_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       rows2::L<true>::kSmem));
+    LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_rows2_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       rows2::L<false>::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_kvf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kvf::kSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_dqf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3349,9 +3655,30 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
   const uint32_t start = P.rows_on ? P.rl_count : 0;
   if (P.rows_on) {
+    const char* r2 = getenv("LLSA_ROWS2");
+    const bool persistent = !(r2 && r2[0] == '0');
+    TmaMaps qmaps{};
+    if (persistent) {
+      const uint64_t in_rows = (uint64_t)units * g.n;
+      if (llsa_status st = make_tma_map(&qmaps.q, q, in_rows, rows2::kQT)) return st;
+      if (llsa_status st = make_tma_map(&qmaps.g, d_out, in_rows, rows2::kQT)) return st;
+    }
     for (uint32_t li = 0; li < P.rl_count; ++li) {
       const uint64_t tasks = (P.rl_tasks[li + 1] - P.rl_tasks[li]) * units;
-      if (P.rl_level[li] >= P.hilo_level)
+      const bool lo = P.rl_level[li] >= P.hilo_level;
+      if (persistent) {
+        const unsigned grid = (unsigned)(tasks < (uint64_t)num_sms() ? tasks : num_sms());
+        if (lo)
+          tc5_rows2_kernel<true><<<grid, rows2::kThreads, rows2::L<true>::kSmem, s>>>(
+              P, qmaps, li, units);
+        else
+          tc5_rows2_kernel<false><<<grid, rows2::kThreads, rows2::L<false>::kSmem, s>>>(
+              P, qmaps, li, units);
+        count_launch();
+        LLSA_LAUNCH_CHECK("tc5_rows2_kernel");
+        continue;
+      }
+      if (lo)
         tc5_kv_rows_kernel<true><<<(unsigned)tasks, 256, rows::Layout<true>::kSmem, s>>>(
             P, li, units);
       else

@@ -130,6 +130,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int x
       "l"(map), "r"(x), "r"(y), "r"(mbar)
       : "memory");
 }
+// 1-D bulk copy global → smem (async proxy); bytes a multiple of 16, both
+// addresses 16-byte aligned; completes `bytes` of transaction on `mbar`.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_map(const void* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(map) : "memory");
 }
