@@ -221,40 +221,38 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
   __syncthreads();
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (uint32_t r = warp; r < B; r += blockDim.x >> 5) {
-    // lane owns positions lane*8 .. lane*8+7 (contiguous → ballot order = position order)
-    float sv[8];
+    // lane owns positions lane*8 .. lane*8+7 (contiguous, so position order =
+    // (lane, i) order).  Scores become order-preserving u32 keys (-0 → +0, the
+    // float compare ties them); each round takes the warp max key with
+    // redux.sync and, among equal keys, the lowest position (topk_row's
+    // lowest-index tie-break), so the selection is exact.
+    uint32_t key[8];
     uint32_t taken = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t c = lane * 8 + i;
-      sv[i] = c < C ? scores[r * 256 + c] : -INFINITY;
+      float v = c < C ? scores[r * 256 + c] : 0.f;
+      if (v == 0.f) v = 0.f;  // canonical +0
+      const uint32_t u = __float_as_uint(v);
+      key[i] = c < C ? ((u & 0x80000000u) ? ~u : (u | 0x80000000u)) : 0u;  // valid keys > 0
     }
-    const uint32_t valid = lane * 8 < C ? ((C - lane * 8 >= 8) ? 0xffu : ((1u << (C - lane * 8)) - 1u)) : 0u;
     for (uint32_t round = 0; round < K; ++round) {
-      float best = 0.f;
-      uint32_t bpos = 0xffffffffu;
+      uint32_t lk = key[0], li = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t c = lane * 8 + i;
-        if (((valid & ~taken) >> i) & 1u) {
-          if (bpos == 0xffffffffu || sv[i] > best) {  // positions ascend: ties keep first
-            best = sv[i];
-            bpos = c;
-          }
+      for (int i = 1; i < 8; ++i)
+        if (key[i] > lk) {
+          lk = key[i];
+          li = i;
         }
-      }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, lk);
+      const uint32_t mypos = lk == mk && lk != 0u ? lane * 8 + li : 0xffffffffu;
+      const uint32_t bpos = __reduce_min_sync(0xffffffffu, mypos);
+      if (bpos == mypos) {
+        taken |= 1u << li;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const uint32_t op = __shfl_xor_sync(0xffffffffu, bpos, o);
-        const bool take = op != 0xffffffffu &&
-                          (bpos == 0xffffffffu || ob > best || (ob == best && op < bpos));
-        if (take) {
-          best = ob;
-          bpos = op;
-        }
+        for (int i = 0; i < 8; ++i)
+          if ((uint32_t)i == li) key[i] = 0u;
       }
-      if (bpos / 8 == lane) taken |= 1u << (bpos % 8);
     }
     const uint32_t cnt = __popc(taken);
     uint32_t pre = cnt;  // inclusive scan of counts
