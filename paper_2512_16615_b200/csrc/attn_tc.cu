@@ -2740,7 +2740,9 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
         const uint32_t s = rc % kRing;
         const uint32_t mc = min(8u, m - ch * 8);
+        if (gi == 0 && lane == 0) trace_ev(p, 1, rc, 0);
         if (rc >= (uint32_t)kRing) mbar_wait(bar(EMPTY + s), ((rc / kRing) - 1) & 1);
+        if (gi == 0 && lane == 0) trace_ev(p, 1, rc, 1);
         const uint32_t st = sbase + s * kStage;
         const uint32_t jj = ch * 8 + lane;
         const uint32_t pre = __shfl_sync(0xffffffffu, ids0, jj & 31);
@@ -2766,6 +2768,7 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
             info[s] = mc | (ch == 0 ? 0x100u : 0u) | (ch + 1 == nch ? 0x200u : 0u);
         }
         cp_async_mbar_arrive(bar(FULL + s));
+        if (gi == 0 && lane == 0) trace_ev(p, 1, rc, 2);
       }
       lo0 = lo1;
       hi0 = hi1;
@@ -2790,6 +2793,7 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         const uint32_t s = c % kRing, b = c & 1;
         mbar_wait(bar(FULL + s), (c / kRing) & 1);
         if (info[s] & 0x400u) break;
+        trace_ev(p, 3, c, 0);
         if (c >= 2) mbar_wait(bar(SFREE + b), ((c >> 1) - 1) & 1);
         fence_proxy_async();  // the gather's cp.async writes → the MMA's async proxy
         fence_after();
@@ -2803,6 +2807,7 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
                    desc_kmajor(st + kVOff + ks * kKStepKMajor), idesc_s, ks > 0);
         }
         commit(bar(SREADY + b));
+        trace_ev(p, 3, c, 1);
       }
     }
   } else if (warp == 13) {
@@ -2819,7 +2824,9 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         if (inf & 0x400u) break;
         const uint32_t mc = inf & 0xFF, first = (inf >> 8) & 1, last = (inf >> 9) & 1;
         const uint32_t ab = ai & 1;
+        trace_ev(p, 6, c, 0);
         mbar_wait(bar(BREADY + b), (c >> 1) & 1);
+        trace_ev(p, 6, c, 1);
         if (first && ai >= 2) mbar_wait(bar(AFREE + ab), ((ai >> 1) - 1) & 1);
         fence_proxy_async();
         fence_after();
@@ -2836,6 +2843,7 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
           commit(bar(AREADY + ab));
           ++ai;
         }
+        trace_ev(p, 6, c, 2);
       }
     }
   } else if (warp >= 3 && warp < 7) {

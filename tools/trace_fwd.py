@@ -32,7 +32,7 @@ for idx, x in enumerate(buf[:cnt]):
     if x >> 63:
         ev.append((idx // 1024, (idx // 32) % 32, idx % 32, x & 0x7FFFFFFFFFFFFFFF))
 t0 = min(e[3] for e in ev)
-names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "MMA", 4: "softmax", 5: "epi"}
+names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "epi", 6: "dKV"}
 ev.sort(key=lambda e: e[3])
 for r, t, e, c in ev:
     if t < 8:
