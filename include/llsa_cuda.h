@@ -111,6 +111,27 @@ llsa_status llsa_pool_backward(const float* d_coarse, uint32_t units,
                                uint32_t block_size, uint32_t hops, float* d_fine,
                                void* stream);
 
+/* ---- 2-D reordering (P/include/llsa/reorder2d.hpp) ------------------------- */
+/* build_reorder, reorder2d.hpp:31-32 (P/src/reorder2d.cpp:11-69): host-side
+ * hierarchical curve for an height x width image, block_size = s^2.  Writes
+ * forward[pos] (raster index at sequence position pos) and inverse[raster]
+ * (height*width entries each, host memory).  NotSquareBlock /
+ * DivisibilityError exactly where the reference throws. */
+llsa_status llsa_build_reorder(uint32_t height, uint32_t width, uint32_t block_size,
+                               uint32_t* forward, uint32_t* inverse);
+/* apply_permutation, reorder2d.hpp:38-39 (reorder2d.cpp:71-88): row gather
+ * out[u][i] = x[u][map[i]] on device (map = forward or inverse, device
+ * memory, `rows` entries); rows of d elements of `dtype`. */
+llsa_status llsa_apply_permutation(const void* x, llsa_dtype dtype, uint32_t units,
+                                   uint64_t rows, uint32_t d, const uint32_t* map, void* out,
+                                   void* stream);
+/* build_pyramid(apply_permutation(x, map)) without materialising the
+ * permuted copy: the gather is fused into level-1 pooling (bit-identical). */
+llsa_status llsa_build_pyramid_permuted(const void* x, llsa_dtype dtype, uint32_t units,
+                                        uint64_t rows, uint32_t d, uint32_t block_size,
+                                        uint32_t levels, const uint32_t* map, float* levels_out,
+                                        void* stream);
+
 /* ---- selection ------------------------------------------------------------ */
 /* select_coarsest, P/include/llsa/selection.hpp:47-50 (selection.cpp:42-79).
  * q_top [units][rows][d], k_top [units][cands][d] → out [units][rows][K]. */

@@ -186,6 +186,7 @@ class OracleC:
                                           C.c_uint32, C.c_float, C.c_uint32, _u32p]
         L.oracle_hierarchical_topk.argtypes = [cfgp, _f32p, _f32p, _u32p,
                                                C.POINTER(C.c_uint64)]
+        L.oracle_build_reorder.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p]
         L.oracle_transpose.argtypes = [_u32p, C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
                                        _u32p]
         L.oracle_build_plan.argtypes = [cfgp, _u32p, _u32p, _u32p, _f32p]
@@ -240,6 +241,12 @@ class OracleC:
                                           parent_level, parent.shape[0], parent.shape[1],
                                           top_k, scale, b, out))
         return out
+
+    def build_reorder(self, h: int, w: int, b: int) -> tuple[int, np.ndarray, np.ndarray]:
+        fwd = np.zeros(max(h * w, 1), np.uint32)
+        inv = np.zeros(max(h * w, 1), np.uint32)
+        code = int(self.lib.oracle_build_reorder(h, w, b, fwd, inv))
+        return code, fwd[:h * w], inv[:h * w]
 
     def transpose(self, idx, key_blocks: int) -> tuple[np.ndarray, np.ndarray]:
         idx = _u32(idx)
@@ -334,6 +341,7 @@ class Reference:
                                        _u32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                        C.c_float, C.c_uint32, _u32p, C.POINTER(C.c_uint64)]
         L.ref_transpose.argtypes = [_u32p, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p]
+        L.ref_build_reorder.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p]
         L.ref_run_pipeline.argtypes = [cfgp, _f32p, _f32p, _f32p] + [opt_f] * 19
         L.ref_oracle_effective.argtypes = [cfgp, _f32p, _f32p, _f32p, _f32p]
         L.ref_oracle_dense.argtypes = [_f32p, _f32p, _f32p, C.c_size_t, C.c_size_t,
@@ -389,6 +397,12 @@ class Reference:
                                             parent, parent_level, parent.shape[0],
                                             parent.shape[1], top_k, scale, b, out, None))
         return out
+
+    def build_reorder(self, h: int, w: int, b: int) -> tuple[int, np.ndarray, np.ndarray]:
+        fwd = np.zeros(max(h * w, 1), np.uint32)
+        inv = np.zeros(max(h * w, 1), np.uint32)
+        code = int(self.lib.ref_build_reorder(h, w, b, fwd, inv))
+        return code, fwd[:h * w], inv[:h * w]
 
     def transpose(self, idx, key_blocks: int) -> tuple[np.ndarray, np.ndarray]:
         idx = _u32(idx)

@@ -677,3 +677,41 @@ uint64_t oracle_input_checksum(const oracle_config* c, const float* q,
   fnv_matrix(&h, v, c->n, c->d);
   return h;
 }
+
+/* build_reorder, P/src/reorder2d.cpp:11-69.  Checks in the reference's order
+ * (:13-30): empty image, non-square block, no patch level (1x1 excepted).
+ * Positions are decoded top-down: the top-level patch row-major across the
+ * image (:46-50), then one base-B digit per sub-patch level (:51-59). */
+int oracle_build_reorder(uint32_t height, uint32_t width, uint32_t block_size,
+                         uint32_t* forward, uint32_t* inverse) {
+  if (height == 0 || width == 0) return 2;
+  uint32_t side = 0;
+  while ((uint64_t)side * side < block_size) ++side;
+  if ((uint64_t)side * side != block_size || block_size == 0) return 12;
+  uint32_t depth = 0;
+  uint64_t patch = 1;
+  while (height % (patch * side) == 0 && width % (patch * side) == 0) {
+    patch *= side;
+    ++depth;
+  }
+  if (depth == 0 && !(height == 1 && width == 1)) return 2;
+  const uint64_t size = (uint64_t)height * width, per_patch = patch * patch;
+  const uint64_t grid_w = width / patch;
+  for (uint64_t pos = 0; pos < size; ++pos) {
+    const uint64_t patch_id = pos / per_patch;
+    uint64_t within = pos % per_patch;
+    uint64_t y = (patch_id / grid_w) * patch, x = (patch_id % grid_w) * patch;
+    uint64_t sub = patch / side;
+    while (sub >= 1 && within > 0) {
+      const uint64_t digit = within / (sub * sub);
+      y += (digit / side) * sub;
+      x += (digit % side) * sub;
+      within %= sub * sub;
+      if (sub == 1) break;
+      sub /= side;
+    }
+    forward[pos] = (uint32_t)(y * width + x);
+  }
+  for (uint64_t pos = 0; pos < size; ++pos) inverse[forward[pos]] = (uint32_t)pos;
+  return 0;
+}

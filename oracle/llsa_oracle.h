@@ -27,6 +27,12 @@
 
 #ifdef __cplusplus
 extern "C" {
+/* build_reorder, P/src/reorder2d.cpp:11-69: the hierarchical 2-D curve
+ * (forward[pos] = raster index, inverse = its inverse).  Returns a status
+ * code (2 DivisibilityError, 12 NotSquareBlock) like the reference throws. */
+int oracle_build_reorder(uint32_t height, uint32_t width, uint32_t block_size,
+                         uint32_t* forward, uint32_t* inverse);
+
 #endif
 
 typedef struct oracle_config {
@@ -77,5 +83,17 @@ uint64_t oracle_input_checksum(const oracle_config* c, const float* q,
 
 #ifdef __cplusplus
 }
+/* build_reorder, P/src/reorder2d.cpp:11-69: the hierarchical 2-D curve
+ * (forward[pos] = raster index, inverse = its inverse).  Returns a status
+ * code (2 DivisibilityError, 12 NotSquareBlock) like the reference throws. */
+int oracle_build_reorder(uint32_t height, uint32_t width, uint32_t block_size,
+                         uint32_t* forward, uint32_t* inverse);
+
 #endif
+/* build_reorder, P/src/reorder2d.cpp:11-69: the hierarchical 2-D curve
+ * (forward[pos] = raster index, inverse = its inverse).  Returns a status
+ * code (2 DivisibilityError, 12 NotSquareBlock) like the reference throws. */
+int oracle_build_reorder(uint32_t height, uint32_t width, uint32_t block_size,
+                         uint32_t* forward, uint32_t* inverse);
+
 #endif

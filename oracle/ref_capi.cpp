@@ -26,6 +26,7 @@
 #include "llsa/oracle.hpp"
 #include "llsa/parallel.hpp"
 #include "llsa/pyramid.hpp"
+#include "llsa/reorder2d.hpp"
 #include "llsa/selection.hpp"
 #include "llsa/tensorio.hpp"
 
@@ -100,6 +101,19 @@ const char* ref_last_error() { return g_err.c_str(); }
 int ref_real_bytes() { return int(sizeof(real)); }
 void ref_set_threads(unsigned t) { set_thread_count(t); }
 unsigned ref_threads() { return thread_count(); }
+
+// build_reorder (reorder2d.cpp:11-69): forward / inverse, height*width each.
+int ref_build_reorder(std::uint32_t h, std::uint32_t w, std::uint32_t b, std::uint32_t* fwd,
+                      std::uint32_t* inv) {
+  try {
+    const Permutation p = build_reorder(h, w, b);
+    std::copy(p.forward.begin(), p.forward.end(), fwd);
+    std::copy(p.inverse.begin(), p.inverse.end(), inv);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
 
 std::uint32_t ref_max_levels(std::uint64_t n, std::uint32_t b) {
   return max_levels(n, b);

@@ -7,10 +7,12 @@ lib/libllsa_cuda.so and raises if it was not built.
 """
 from . import _lib
 from ._lib import (ArgumentError, ConfigError, CudaError, DivisibilityError, Error,
-                   IndexOutOfRange, LevelError, NonFiniteError, ShapeMismatch, StaleState,
+                   IndexOutOfRange, LevelError, NonFiniteError, NotSquareBlock, ShapeMismatch,
+                   StaleState,
                    TopKError, Unsupported)
-from .ops import (ForwardState, LLSAConfig, LLSAHandle, ValidatedConfig, build_plan,
-                  build_pyramid, dump_selection, effective_block_count, hierarchical_topk,
+from .ops import (ForwardState, LLSAConfig, LLSAHandle, ValidatedConfig, apply_permutation,
+                  build_plan, build_pyramid, build_pyramid_permuted, build_reorder,
+                  dump_selection, effective_block_count, hierarchical_topk,
                   kv_backward, llsa_backward, llsa_forward, max_levels, pool_backward,
                   pyramid_levels, select_coarsest, select_level, split_tables, sync_status,
                   transpose_all, transpose_indices, validate_config)

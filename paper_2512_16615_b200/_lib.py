@@ -77,6 +77,10 @@ SIGNATURES = {
     "llsa_backward_mul_accs": (_u64, [_cfgp]),
     "llsa_build_pyramid": (C.c_int, [_vp, C.c_int, _u32, _u64, _u32, _u32, _u32, _vp, _vp]),
     "llsa_pool_backward": (C.c_int, [_vp, _u32, _u64, _u32, _u32, _u32, _vp, _vp]),
+    "llsa_build_reorder": (C.c_int, [_u32, _u32, _u32, _vp, _vp]),
+    "llsa_apply_permutation": (C.c_int, [_vp, C.c_int, _u32, _u64, _u32, _vp, _vp, _vp]),
+    "llsa_build_pyramid_permuted": (C.c_int, [_vp, C.c_int, _u32, _u64, _u32, _u32, _u32, _vp,
+                                              _vp, _vp]),
     "llsa_select_coarsest": (C.c_int, [_vp, _vp, _u32, _u32, _u32, _u32, _u32, _f32, _vp, _vp]),
     "llsa_select_level": (C.c_int, [_vp, _vp, _vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32,
                                     _f32, _u32, _vp, _vp]),

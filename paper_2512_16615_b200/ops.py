@@ -180,6 +180,52 @@ def pyramid_levels(flat: torch.Tensor, n: int, block_size: int, levels: int) -> 
     return out
 
 
+def build_reorder(height: int, width: int, block_size: int):
+    """build_reorder, reorder2d.hpp:31-32: the hierarchical 2-D curve.
+    Returns ``(forward, inverse)`` as uint32 numpy arrays of height*width
+    entries (forward[pos] = raster index at sequence position pos)."""
+    import numpy as np
+    lib = _lib.load()
+    size = int(height) * int(width)
+    fwd = np.empty(max(size, 1), dtype=np.uint32)
+    inv = np.empty(max(size, 1), dtype=np.uint32)
+    check(lib.llsa_build_reorder(height, width, block_size, fwd.ctypes.data, inv.ctypes.data))
+    return fwd[:size], inv[:size]
+
+
+def apply_permutation(x: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    """apply_permutation, reorder2d.hpp:38-39: ``out[..., i, :] = x[..., perm[i], :]``
+    per unit, on the GPU (``perm`` = forward for raster → sequence order,
+    inverse to undo it)."""
+    lib = _lib.load()
+    xu = _as_units(x, "x")
+    units, rows, d = xu.shape
+    m = perm.to(device=xu.device, dtype=torch.int32).contiguous()
+    if m.numel() != rows:
+        raise _lib.ShapeMismatch(f"matrix has {rows} rows, permutation covers {m.numel()}")
+    out = torch.empty_like(xu)
+    check(lib.llsa_apply_permutation(_ptr(xu), _dtype_code(xu), units, rows, d, _ptr(m),
+                                     _ptr(out), _stream()))
+    return out.view(x.shape)
+
+
+def build_pyramid_permuted(x: torch.Tensor, perm: torch.Tensor, block_size: int,
+                           levels: int) -> torch.Tensor:
+    """``build_pyramid(apply_permutation(x, perm))`` with the gather fused into
+    the level-1 pooling (no permuted copy of ``x`` is written)."""
+    lib = _lib.load()
+    xu = _as_units(x, "x")
+    units, rows, d = xu.shape
+    m = perm.to(device=xu.device, dtype=torch.int32).contiguous()
+    if m.numel() != rows:
+        raise _lib.ShapeMismatch(f"matrix has {rows} rows, permutation covers {m.numel()}")
+    pr = int(lib.llsa_pyramid_rows(rows, block_size, levels))
+    out = torch.empty((units, max(pr, 0), d), device=xu.device, dtype=torch.float32)
+    check(lib.llsa_build_pyramid_permuted(_ptr(xu), _dtype_code(xu), units, rows, d, block_size,
+                                          levels, _ptr(m), _ptr(out), _stream()))
+    return out
+
+
 def pool_backward(d_coarse: torch.Tensor, block_size: int, hops: int) -> torch.Tensor:
     """pool_backward, pyramid.hpp:31-32."""
     lib = _lib.load()

@@ -37,7 +37,8 @@ FP32_TOLERANCE_CASES = {
 # suites are linked against it (oracle/Makefile `reftests32`, recorded in
 # tests/golden/ref_f32_suite_failures.json).
 CPU_SUITES = ("core", "tensorio")
-GPU_SUITES = ("pyramid", "selection", "indexmap", "attention", "attention_grad", "oracle")
+GPU_SUITES = ("pyramid", "selection", "indexmap", "attention", "attention_grad", "oracle",
+              "reorder2d")
 
 
 def _run(suite):
