@@ -240,6 +240,21 @@ llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units,
                              float* dk, float* dv, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* mask_kv_backward, P/include/llsa/oracle.hpp:54-63 (P/src/oracle.cpp:365-501):
+ * the measured baseline of the key/value backward.  The key→query lookup
+ * goes through a dense query-block × key-block mask per level (O(T^2) build
+ * and column scan) instead of the CSC; same math and kernels otherwise.
+ * tables as produced by llsa_hierarchical_topk. */
+size_t llsa_mask_kv_backward_workspace_bytes(const llsa_config* cfg, uint32_t units);
+llsa_status llsa_mask_kv_backward(const llsa_config* cfg, uint32_t units,
+                                  llsa_dtype dtype, const void* d_out,
+                                  const float* out, const float* row_max,
+                                  const float* row_denom, const void* q,
+                                  const float* pyr_k, const float* pyr_v,
+                                  const void* k, const void* v, const uint32_t* tables,
+                                  float* dk, float* dv, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ---- fused path (the B200 fast path; one handle owns all scratch) ---------- */
 /* A handle caches the per-unit pyramids, tables, CSC lists, softmax
  * statistics and every intermediate of the path for `units` units of one

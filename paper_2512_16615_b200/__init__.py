@@ -13,7 +13,7 @@ from ._lib import (ArgumentError, ConfigError, CudaError, DivisibilityError, Err
 from .ops import (ForwardState, LLSAConfig, LLSAHandle, ValidatedConfig, apply_permutation,
                   build_plan, build_pyramid, build_pyramid_permuted, build_reorder,
                   dump_selection, effective_block_count, hierarchical_topk,
-                  kv_backward, llsa_backward, llsa_forward, max_levels, pool_backward,
+                  kv_backward, llsa_backward, llsa_forward, mask_kv_backward, max_levels, pool_backward,
                   pyramid_levels, select_coarsest, select_level, split_tables, sync_status,
                   transpose_all, transpose_indices, validate_config)
 

@@ -98,6 +98,8 @@ SIGNATURES = {
     "llsa_backward_workspace_bytes": (_sz, [_cfgp, _u32]),
     "llsa_backward": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 16 + [_sz, _vp]),
     "llsa_kv_backward": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 14 + [_sz, _vp]),
+    "llsa_mask_kv_backward_workspace_bytes": (_sz, [_cfgp, _u32]),
+    "llsa_mask_kv_backward": (C.c_int, [_cfgp, _u32, C.c_int] + [_vp] * 13 + [_sz, _vp]),
     "llsa_handle_create": (C.c_int, [_cfgp, _u32, C.c_int, C.POINTER(_vp)]),
     "llsa_handle_destroy": (C.c_int, [_vp]),
     "llsa_handle_uses_tensor_cores": (C.c_int, [_vp]),

@@ -588,6 +588,57 @@ llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units, llsa_dtype 
                        flat, nullptr, dk, dv, ws, S(stream));
 }
 
+namespace {
+size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+size_t mask_kv_ws(const Geometry& g, uint32_t units) {
+  return al256((size_t)units * g.csc_off_entries * 4) +
+         al256((size_t)units * g.csc_flat_entries * 4) + al256(mask_lookup_ws_bytes(g, units)) +
+         al256(simt_backward_ws_bytes(g, units));
+}
+}  // namespace
+
+size_t llsa_mask_kv_backward_workspace_bytes(const llsa_config* cfg, uint32_t units) {
+  Geometry g;
+  if (make_geometry(cfg, &g)) return 0;
+  return mask_kv_ws(g, units);
+}
+
+llsa_status llsa_mask_kv_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
+                                  const void* d_out, const float* out, const float* rm,
+                                  const float* rd, const void* q, const float* pyr_k,
+                                  const float* pyr_v, const void* k, const void* v,
+                                  const uint32_t* tables, float* dk, float* dv, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  Geometry g;
+  if (llsa_status st = make_geometry(cfg, &g)) return st;
+  if (llsa_status st = dtype_ok(dt)) return st;
+  if (units == 0) return LLSA_OK;
+  NONNULL(d_out);
+  NONNULL(out);
+  NONNULL(rm);
+  NONNULL(rd);
+  NONNULL(q);
+  NONNULL(k);
+  NONNULL(v);
+  NONNULL(pyr_k);
+  NONNULL(pyr_v);
+  NONNULL(tables);
+  NONNULL(dk);
+  NONNULL(dv);
+  if (!ws || ws_bytes < mask_kv_ws(g, units))
+    return fail(LLSA_ERR_ARGUMENT, "mask kv-backward workspace too small");
+  char* p = static_cast<char*>(ws);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(p);
+  p += al256((size_t)units * g.csc_off_entries * 4);
+  uint32_t* flat = reinterpret_cast<uint32_t*>(p);
+  p += al256((size_t)units * g.csc_flat_entries * 4);
+  void* mws = p;
+  p += al256(mask_lookup_ws_bytes(g, units));
+  if (llsa_status st = mask_lookup(g, units, tables, offs, flat, mws, S(stream))) return st;
+  return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, nullptr, offs,
+                       flat, nullptr, dk, dv, p, S(stream));
+}
+
 // ---------------------------------------------------------------------------
 // Handle (fused) API
 // ---------------------------------------------------------------------------

@@ -68,6 +68,10 @@ void count_launch(uint32_t n = 1);
 uint32_t take_launch_count();
 
 // ---- launchers (each returns LLSA_OK or an error; no synchronisation) ----
+// Mask-based key→query lookup (transpose.cu): the kv-backward baseline
+size_t mask_lookup_ws_bytes(const Geometry& g, uint32_t units);
+llsa_status mask_lookup(const Geometry& g, uint32_t units, const uint32_t* tables,
+                        uint32_t* offs, uint32_t* flat, void* ws, cudaStream_t s);
 // CSR → CSC of every selection level in four launches (transpose.cu)
 bool transpose_all_fused_ok(const Geometry& g);
 size_t transpose_all_fused_ws(const Geometry& g, uint32_t units);

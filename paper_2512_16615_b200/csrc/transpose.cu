@@ -343,3 +343,158 @@ llsa_status transpose_all_fused(const Geometry& g, uint32_t units, const uint32_
 }
 
 }  // namespace llsa_impl
+
+// ---------------------------------------------------------------------------
+// Mask-based key→query lookup: the measured baseline of the key/value
+// backward (SURVEY.md §8(f) row 2, P/src/oracle.cpp:365-501).  Per level a
+// dense query-block × key-block bit mask is built from the tables, and every
+// key block scans its whole mask column — O(T_q·T_k) per level instead of
+// the CSR→CSC pass's O(T·K).  The column scan visits rows in ascending order,
+// so it emits the same canonical CSC as llsa_transpose_all and the same
+// key-major backward kernels then consume it.
+// ---------------------------------------------------------------------------
+namespace llsa_impl {
+namespace {
+
+struct MaskAll {
+  const uint32_t* idx[kTrMax];
+  uint32_t* mask[kTrMax];   // [units][T_q][words]
+  uint32_t* offs[kTrMax];
+  uint32_t* flat[kTrMax];
+  uint32_t rows[kTrMax], kb[kTrMax], words[kTrMax];
+  uint64_t idx_stride, off_stride, flat_stride, mask_stride[kTrMax];
+  uint32_t units, k;
+  uint32_t* flag;
+};
+
+__global__ void mask_build_kernel(MaskAll a) {
+  const uint32_t l = blockIdx.y;
+  const uint64_t per_unit = (uint64_t)a.rows[l] * a.k, total = per_unit * a.units;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e / per_unit, i = e - u * per_unit, row = i / a.k;
+    const uint32_t b = a.idx[l][u * a.idx_stride + i];
+    if (b >= a.kb[l]) {
+      raise_flag(a.flag, kErrIndex);
+      continue;
+    }
+    atomicOr(&a.mask[l][u * a.mask_stride[l] + row * a.words[l] + (b >> 5)], 1u << (b & 31));
+  }
+}
+
+// thread = (unit, key block): count (pass 0) or emit (pass 1) its column.
+__global__ void mask_scan_kernel(MaskAll a, int pass) {
+  const uint32_t l = blockIdx.y;
+  const uint64_t total = (uint64_t)a.kb[l] * a.units;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = t / a.kb[l], b = t - u * a.kb[l];
+    const uint32_t* m = a.mask[l] + u * a.mask_stride[l] + (b >> 5);
+    const uint32_t bit = 1u << (b & 31);
+    uint32_t* off = a.offs[l] + u * a.off_stride;
+    if (pass == 0) {
+      uint32_t c = 0;
+      for (uint32_t i = 0; i < a.rows[l]; ++i) c += (m[(uint64_t)i * a.words[l]] & bit) ? 1u : 0u;
+      off[b] = c;  // count, turned into offsets by the scan
+    } else {
+      uint32_t* dst = a.flat[l] + u * a.flat_stride + off[b];
+      for (uint32_t i = 0; i < a.rows[l]; ++i)
+        if (m[(uint64_t)i * a.words[l]] & bit) *dst++ = i;
+    }
+  }
+}
+
+// in-place exclusive scan of counts[0..kb) → offsets[0..kb]; CTA = (unit, level)
+__global__ void __launch_bounds__(1024) mask_offsets_kernel(MaskAll a) {
+  const uint32_t l = blockIdx.y, u = blockIdx.x, kbn = a.kb[l];
+  uint32_t* off = a.offs[l] + (uint64_t)u * a.off_stride;
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t base = 0; base < kbn; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < kbn ? off[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= (uint32_t)o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid ? warp_tot[wid - 1] : 0u) + x - v;
+    if (i < kbn) off[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[kbn] = carry;
+}
+
+}  // namespace
+
+size_t mask_lookup_ws_bytes(const Geometry& g, uint32_t units) {
+  size_t b = 256;
+  for (uint32_t l = 0; l < g.L && l < (uint32_t)kTrMax; ++l)
+    b += ((size_t)units * g.level_blocks(l) * ((g.level_blocks(l) + 31) / 32) * 4 + 255) &
+         ~size_t(255);
+  return b;
+}
+
+llsa_status mask_lookup(const Geometry& g, uint32_t units, const uint32_t* tables,
+                        uint32_t* offs, uint32_t* flat, void* ws, cudaStream_t s) {
+  if (g.L > (uint32_t)kTrMax) return fail(LLSA_ERR_UNSUPPORTED, "too many levels");
+  MaskAll a{};
+  char* p = static_cast<char*>(ws);
+  size_t mb = 0;
+  uint64_t maxe = 0, maxkb = 0;
+  for (uint32_t l = 0; l < g.L; ++l) {
+    const uint64_t t = g.level_blocks(l);
+    a.words[l] = (uint32_t)((t + 31) / 32);
+    a.mask_stride[l] = t * a.words[l];
+    a.mask[l] = reinterpret_cast<uint32_t*>(p + mb);
+    mb += ((size_t)units * a.mask_stride[l] * 4 + 255) & ~size_t(255);
+    a.idx[l] = tables + g.table_off[l];
+    a.offs[l] = offs + g.csc_off_off[l];
+    a.flat[l] = flat + g.csc_flat_off[l];
+    a.rows[l] = (uint32_t)t;
+    a.kb[l] = (uint32_t)t;
+    maxe = t * g.K > maxe ? t * g.K : maxe;
+    maxkb = t > maxkb ? t : maxkb;
+  }
+  a.idx_stride = g.table_entries;
+  a.off_stride = g.csc_off_entries;
+  a.flat_stride = g.csc_flat_entries;
+  a.units = units;
+  a.k = g.K;
+  a.flag = device_flag();
+  LLSA_CUDA_TRY(cudaMemsetAsync(ws, 0, mb, s));
+  mask_build_kernel<<<dim3(grid_for(maxe * units, 256), g.L), 256, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("mask_build_kernel");
+  const dim3 gs(grid_for(maxkb * units, 128), g.L);
+  mask_scan_kernel<<<gs, 128, 0, s>>>(a, 0);
+  count_launch();
+  LLSA_LAUNCH_CHECK("mask_scan_kernel");
+  mask_offsets_kernel<<<dim3(units, g.L), 1024, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("mask_offsets_kernel");
+  mask_scan_kernel<<<gs, 128, 0, s>>>(a, 1);
+  count_launch();
+  LLSA_LAUNCH_CHECK("mask_scan_kernel");
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl

@@ -460,6 +460,31 @@ def kv_backward(d_out, state: ForwardState, q, k, v, pyr_k, pyr_v, transposed,
     return dk, dv
 
 
+def mask_kv_backward(d_out, state: ForwardState, q, k, v, pyr_k, pyr_v, tables,
+                     cfg: ValidatedConfig) -> tuple:
+    """mask_kv_backward, oracle.hpp:54-63 → (dk, dv) fp32: the kv backward with
+    the key→query lookup through dense per-level block masks (the measured
+    baseline of the CSC path; same result)."""
+    lib = _lib.load()
+    q, k, v = (_as_units(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v")))
+    _check_qkv(q, k, v, cfg)
+    dO = _as_units(d_out, "d_out").to(q.dtype)
+    units = q.shape[0]
+    dk, dv = (torch.empty((units, cfg.n, cfg.d), device=q.device, dtype=torch.float32)
+              for _ in range(2))
+    wsb = int(lib.llsa_mask_kv_backward_workspace_bytes(C.byref(cfg.c()), units))
+    ws = torch.empty(wsb, device=q.device, dtype=torch.uint8)
+    check(lib.llsa_mask_kv_backward(C.byref(cfg.c()), units, _dtype_code(q), _ptr(dO),
+                                    _ptr(_as_units(state.output, "output")),
+                                    _ptr(state.row_max.contiguous()),
+                                    _ptr(state.row_denom.contiguous()), _ptr(q),
+                                    _ptr(_as_units(pyr_k, "pyr_k")),
+                                    _ptr(_as_units(pyr_v, "pyr_v")), _ptr(k), _ptr(v),
+                                    _ptr(tables.contiguous()), _ptr(dk), _ptr(dv), _ptr(ws), wsb,
+                                    _stream()))
+    return dk, dv
+
+
 # --------------------------------------------------------------------------
 # fused path
 # --------------------------------------------------------------------------

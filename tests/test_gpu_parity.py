@@ -225,6 +225,10 @@ def test_staged_path_matches_oracle(oracle_c, cfg, bf):
         assert e["max_rel"] <= 1e-3, (name, e)
     dk2, dv2 = llsa.kv_backward(tdo, st, tq, tk, tv, pk, pv, tr, vc)
     assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
+    # the mask-based baseline (oracle.cpp:365-501) finds the same key→query
+    # lists through dense block masks, so it reproduces the CSC path exactly
+    dk3, dv3 = llsa.mask_kv_backward(tdo, st, tq, tk, tv, pk, pv, tables, vc)
+    assert torch.equal(dk3, dk) and torch.equal(dv3, dv)
 
 
 def test_forward_overflow_without_rescaling_raises():
