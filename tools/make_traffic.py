@@ -13,9 +13,10 @@ import sys
 STAGES = {  # bench stage -> kernel name prefixes (one launch each per step)
     "fwd_attention": ["tc5_fwd_kernel"],
     "bwd_dq": ["tc5_dqf_kernel"],
-    "bwd_kv_coarse_tc5": ["tc5_kv_rows_kernel<0>", "tc5_kv_rows_kernel<1>", "rows_reduce_kernel"],
+    "bwd_kv_coarse_tc5": ["tc5_rows2_kernel<0>", "tc5_rows2_kernel<1>", "rows_reduce_kernel"],
+    "compress": ["pyr12_kernel"],
     "bwd_kv_coarse": ["tc_kv_kernel<2>", "reduce_parts_kernel"],
-    "bwd_kv_fine": ["tc_kv_kernel<0>"],
+    "bwd_kv_fine": ["tc5_kvf_kernel"],
     "select": ["select_coarsest_kernel", "select_level_fast_kernel<8>"],
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}

@@ -14,7 +14,7 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[1]
 ia, isrc, ist = hdr.index("Address"), hdr.index("Source"), hdr.index(
     "Warp Stall Sampling (All Samples)")
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+body = [r for r in rows[2:] if len(r) == len(hdr) and r[ist].isdigit()]
 tot = sum(int(r[ist]) for r in body)
 print("total samples", tot, "instructions", len(body))
 for i, r in sorted(enumerate(body), key=lambda x: -int(x[1][ist]))[:n]:

@@ -14,7 +14,7 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[1]
 isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
 ist = hdr.index("Warp Stall Sampling (All Samples)")
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+body = [r for r in rows[2:] if len(r) == len(hdr) and r[ist].isdigit()]
 c = collections.Counter()
 st = collections.Counter()
 for r in body[lo:hi]:

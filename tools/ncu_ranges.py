@@ -16,7 +16,7 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[1]
 isrc, ist = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 iex = hdr.index("Instructions Executed")
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+body = [r for r in rows[2:] if len(r) == len(hdr) and r[ist].isdigit()]
 tot = sum(int(r[ist]) for r in body)
 KEY = ("HMMA", "UTCHMMA", "UTCBAR", "LDTM", "MUFU", "SYNCS", "LDGSTS", "UTMALDG", "STS", "LDSM",
        "STG", "BAR", "LDG", "F2FP")
