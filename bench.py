@@ -258,6 +258,8 @@ def main() -> None:
                          "for BASELINE C4 = batch 8 x 16 heads)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of a captured CUDA graph")
     ap.add_argument("--no-dense", action="store_true",
                     help="skip the dense SDPA comparator")
     args = ap.parse_args()
@@ -333,20 +335,46 @@ def main() -> None:
     for _ in range(args.warmup):
         launches = step()
     llsa.sync_status()
-    h.enable_timing(True)  # reset the event ring: stage times cover the timed region only
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # per-stage breakdown: an eager pass with the handle's stage events on
+    h.enable_timing(True)  # reset the event ring
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1) / args.steps
+    stages = h.stage_times()
+    llsa.sync_status()
+
+    # the timed region: the step's launch sequence captured once as a CUDA
+    # graph and replayed (static shapes, as in a training loop), which
+    # removes the host launch gaps between the ~30 kernels of a step
+    graph = None
+    if not args.no_graph:
+        h.enable_timing(False)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        llsa.sync_status()
 
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            launches = step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    stages = h.stage_times()
     llsa.sync_status()
     from paper_2512_16615_b200.sharding import max_over_ranks
     ms = max_over_ranks(ms)
@@ -477,6 +505,8 @@ def main() -> None:
                 "ideal_ms": ideal_ms,
                 "roofline": roof,
                 "stages_ms": {s: round(t_, 4) for s, t_ in stages},
+                "eager_ms_per_step": eager_ms,
+                "timed_launch_mode": "cuda_graph_replay" if graph is not None else "eager",
                 "tensor_cores": h.uses_tensor_cores,
                 "cpu_baseline": cpu, "e2e": e2e, "dense_sdpa": dense, "gpu_launches": launches * args.steps,
                 "clocks": clk.summary()}
