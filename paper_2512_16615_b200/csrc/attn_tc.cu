@@ -2225,22 +2225,24 @@ namespace dqf {
 constexpr int kTileBytes = kTileQ * 128;        // 16 KB
 constexpr int kCStage = 4 * 8192;               // Khi, Klo, Vhi, Vlo of 64 keys
 constexpr int kCRing = 2;
+constexpr int kQS = 1;                          // Q/dO stages
 constexpr int kDSBytes = kTileQ * 128;          // dS chunk: 128 rows x 64 keys bf16
-constexpr int kFineWarp = 2 * 4096;             // 2 stages of one {K, V} block
-constexpr int kOffQ = 0, kOffG = kTileBytes;
-constexpr int kOffC = 2 * kTileBytes;                     // 32 KB
-constexpr int kOffDS = kOffC + kCRing * kCStage;          // 96 KB
-constexpr int kOffFine = kOffDS + 2 * kDSBytes;           // 128 KB
-constexpr int kOffDQf = kOffFine + 8 * kFineWarp;         // 192 KB: dQ_f [128][64] fp32
-constexpr int kOffStat = kOffDQf + kTileQ * kD * 4;       // 224 KB: lse, D x 2 tiles
+constexpr int kFS = 3;                          // fine ring stages per warp
+constexpr int kFineWarp = kFS * 4096;           // {K, V} block per stage
+constexpr int kQStage = 2 * kTileBytes;                   // Q | dO of one tile
+constexpr int kOffQ = 0;
+constexpr int kOffC = kQS * kQStage;
+constexpr int kOffDS = kOffC + kCRing * kCStage;
+constexpr int kOffFine = kOffDS + 2 * kDSBytes;
+constexpr int kOffStat = kOffFine + 8 * kFineWarp;        // lse, D x 2 tiles
 constexpr int kOffEnt = kOffStat + 4 * kTileQ * 4;        // bias[32], chunk info[8], rows[32]
 constexpr int kOffBar = kOffEnt + 256;
-enum { QFULL = 0, QEMPTY = 1, KFULL = 2, KEMPTY = 4, SREADY = 6, TFREE = 8, DSREADY = 10,
-       DSFREE = 12, DQREADY = 14, DQFREE = 16, DREADY = 18, FDONE = 20, FFREE = 21,
-       NBAR = 22 };
+enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 7, SREADY = 10, TFREE = 12, DSREADY = 14,
+       DSFREE = 16, DQREADY = 18, DQFREE = 20, DREADY = 22, FDONE = 24, FFREE = 26,
+       NBAR = 28 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
 constexpr int kThreads = 16 * 32;
-constexpr uint32_t kTmemCols = 512;  // S/dP x 2 buffers [0, 256), dQ_c x 2 [256, 384)
+constexpr uint32_t kTmemCols = 512;  // S/dP x 2 [0, 256), dQ_c x 2 [256, 384), dQ_f x 2 [384, 512)
 constexpr uint32_t kMaxEntries = 24;  // ent_rows[24]
 }  // namespace dqf
 
@@ -2261,7 +2263,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
   float* stat = reinterpret_cast<float*>(smem + kOffStat);  // [2 tiles][lse | D][128]
-  float* dqs = reinterpret_cast<float*>(smem + kOffDQf);
   float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
   uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
   uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 160);  // [24]
@@ -2277,11 +2278,15 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   }
   if (warp == 0) tmem_alloc(smem_u32(tslot), kTmemCols);
   if (tid == 0) {
-    mbar_init(bar(QFULL), 1);
-    mbar_init(bar(QEMPTY), 1);  // S/dP MMAs of the tile done
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kCRing; ++i) {
       mbar_init(bar(KFULL + i), 32);  // every gather lane, via its copies
       mbar_init(bar(KEMPTY + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(QFULL + i), 1);
+      mbar_init(bar(QEMPTY + i), 1);  // S/dP MMAs of the tile done
+      mbar_init(bar(FDONE + i), 256);
+      mbar_init(bar(FFREE + i), 128);
       mbar_init(bar(SREADY + i), 1);
       mbar_init(bar(TFREE + i), 128);
       mbar_init(bar(DSREADY + i), 128);
@@ -2290,8 +2295,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       mbar_init(bar(DQFREE + i), 128);
       mbar_init(bar(DREADY + i), 256);
     }
-    mbar_init(bar(FDONE), 256);
-    mbar_init(bar(FFREE), 128);
     fence_mbar_init();
   }
   fence_before();
@@ -2309,10 +2312,13 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
         const uint32_t unit = (uint32_t)(id / tpu);
         const uint64_t q0 = (id % tpu) * kTileQ;
-        if (i >= 1) mbar_wait(bar(QEMPTY), (i - 1) & 1);
-        mbar_expect_tx(bar(QFULL), 2 * kTileBytes);
-        tma_load_2d(sbase + kOffQ, &m.q, 0, (int)(unit * p.n + q0), bar(QFULL));
-        tma_load_2d(sbase + kOffG, &m.g, 0, (int)(unit * p.n + q0), bar(QFULL));
+        const uint32_t qs = i % kQS;
+        if (i >= (uint32_t)kQS) mbar_wait(bar(QEMPTY + qs), ((i / kQS) - 1) & 1);
+        mbar_expect_tx(bar(QFULL + qs), kQStage);
+        tma_load_2d(sbase + kOffQ + qs * kQStage, &m.q, 0, (int)(unit * p.n + q0),
+                    bar(QFULL + qs));
+        tma_load_2d(sbase + kOffQ + qs * kQStage + kTileBytes, &m.g, 0, (int)(unit * p.n + q0),
+                    bar(QFULL + qs));
       }
     }
   } else if (warp == 0) {
@@ -2338,7 +2344,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         const uint32_t s = rc % kCRing;
         const uint32_t info = ch_info[ch], ne = info & 0xFF;
         const bool lo = info & 0x100u;
+        if (lane == 0) trace_ev(p, 1, rc, 0);
         if (rc >= (uint32_t)kCRing) mbar_wait(bar(KEMPTY + s), ((rc / kCRing) - 1) & 1);
+        if (lane == 0) trace_ev(p, 1, rc, 1);
         const uint32_t dst = sbase + kOffC + s * kCStage;
         for (uint32_t e = 0; e < ne; ++e) {
           const uint64_t o = (uint64_t)__shfl_sync(0xffffffffu, myrow, ch * 4 + e) * kD;
@@ -2357,8 +2365,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
     if (lane == 0) {
       uint32_t c = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-        mbar_wait(bar(QFULL), i & 1);
-        const uint32_t sq = sbase + kOffQ, sg = sbase + kOffG;
+        const uint32_t qs = i % kQS;
+        mbar_wait(bar(QFULL + qs), (i / kQS) & 1);
+        const uint32_t sq = sbase + kOffQ + qs * kQStage, sg = sq + kTileBytes;
         for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
           const uint32_t s = c % kCRing, b = c & 1;
           mbar_wait(bar(KFULL + s), (c / kCRing) & 1);
@@ -2382,7 +2391,8 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             }
           }
           commit(bar(SREADY + b));
-          if (ch + 1 == nch) commit(bar(QEMPTY));
+          trace_ev(p, 3, c, 0);
+          if (ch + 1 == nch) commit(bar(QEMPTY + qs));
         }
       }
     }
@@ -2409,6 +2419,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
                      (ch == 0 && ks == 0) ? 0u : 1u);
           commit(bar(KEMPTY + s));
           commit(bar(DSFREE + b));
+          trace_ev(p, 6, c, 0);
           if (ch + 1 == nch) commit(bar(DQREADY + tb));
         }
       }
@@ -2465,36 +2476,41 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         mbar_arrive(bar(TFREE + b));
         fence_proxy_async();
         mbar_arrive(bar(DSREADY + b));
+        if (tid == 96) trace_ev(p, 4, c, 0);
       }
       // tile epilogue: dq = scale (dQ_c + dQ_f), written once
+      if (tid == 96) trace_ev(p, 7, i, 0);
       mbar_wait(bar(DQREADY + tb), (i >> 1) & 1);
-      mbar_wait(bar(FDONE), i & 1);
+      if (tid == 96) trace_ev(p, 7, i, 1);
+      mbar_wait(bar(FDONE + tb), (i >> 1) & 1);
+      if (tid == 96) trace_ev(p, 7, i, 2);
       fence_after();
       float* d = p.dq + ((uint64_t)unit * p.n + q0 + row) * kD;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t r0[32];
-        tmem_ld32(tmem + lane_off + 256 + tb * 64 + 32 * hh, r0);
+        uint32_t r0[32], f[32];
+        tmem_ld32(tmem + lane_off + 256 + tb * 64 + 32 * hh, r0);   // dQ_c
+        tmem_ld32(tmem + lane_off + 384 + tb * 64 + 32 * hh, f);    // dQ_f (fine warps)
         tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float4 f =
-              *reinterpret_cast<const float4*>(dqs + dqf_idx(row, 32 * hh + 4 * k));
           float4 v;
-          v.x = (__uint_as_float(r0[4 * k]) + f.x) * p.scale;
-          v.y = (__uint_as_float(r0[4 * k + 1]) + f.y) * p.scale;
-          v.z = (__uint_as_float(r0[4 * k + 2]) + f.z) * p.scale;
-          v.w = (__uint_as_float(r0[4 * k + 3]) + f.w) * p.scale;
+          v.x = (__uint_as_float(r0[4 * k]) + __uint_as_float(f[4 * k])) * p.scale;
+          v.y = (__uint_as_float(r0[4 * k + 1]) + __uint_as_float(f[4 * k + 1])) * p.scale;
+          v.z = (__uint_as_float(r0[4 * k + 2]) + __uint_as_float(f[4 * k + 2])) * p.scale;
+          v.w = (__uint_as_float(r0[4 * k + 3]) + __uint_as_float(f[4 * k + 3])) * p.scale;
           reinterpret_cast<float4*>(d + 32 * hh)[k] = v;
         }
       }
       fence_before();
       mbar_arrive(bar(DQFREE + tb));
-      mbar_arrive(bar(FFREE));
+      mbar_arrive(bar(FFREE + tb));
     }
   } else if (warp >= 7) {
     // ------------------------------------------------------------ fine warps
-    const uint32_t fw = warp - 7;
+    // fine block of this warp: its 16 rows must be TMEM lanes of the warp's
+    // sub-partition (warp % 4), where it stages its dQ part
+    const uint32_t fw = 2 * (warp & 3) + (warp >= 11 ? 1u : 0u);
     const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
     const uint64_t nfb = p.n / kBS;
     const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
@@ -2519,14 +2535,18 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           raise_flag(p.flag, llsa_dev::kErrIndex);
           b = 0;
         }
-        const uint32_t base = sF + (j & 1) * 4096;
+        const uint32_t base = sF + (j % kFS) * 4096;
         load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
         load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
       };
-      // this warp's own 16 Q and dO rows go to ring stage 1 (free until block 1)
-      load_fine(0);
-      load_block16_async(sF + 4096, p.q + in_off + (q0 + fw * 16) * kD, bl, lane);
-      load_block16_async(sF + 4096 + kTile16, p.dout + in_off + (q0 + fw * 16) * kD, bl, lane);
+      // blocks 0 .. kFS-2 prefetched; this warp's own 16 Q and dO rows go to
+      // the last ring stage (free until block kFS-1 is loaded)
+      constexpr uint32_t sQD = (kFS - 1) * 4096;
+#pragma unroll
+      for (uint32_t j = 0; j + 1 < (uint32_t)kFS; ++j)
+        if (j < p.K) load_fine(j);
+      load_block16_async(sF + sQD, p.q + in_off + (q0 + fw * 16) * kD, bl, lane);
+      load_block16_async(sF + sQD + kTile16, p.dout + in_off + (q0 + fw * 16) * kD, bl, lane);
       cp_async_commit();
       next_ids = fine_ids(id + gridDim.x);
       // D = rowsum(dO∘O) (fp32 O) and the log2 LSE of this warp's 16 rows;
@@ -2546,8 +2566,8 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       uint32_t qf[4][4], gf[4][4];
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        lda(sF + 4096, 0, ks, lane, qf[ks]);
-        lda(sF + 4096 + kTile16, 0, ks, lane, gf[ks]);
+        lda(sF + sQD, 0, ks, lane, qf[ks]);
+        lda(sF + sQD + kTile16, 0, ks, lane, gf[ks]);
       }
       float dsum = 0.f;
 #pragma unroll
@@ -2555,7 +2575,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         uint4 gv;
         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n"
                      : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
-                     : "r"(sF + 4096 + kTile16 + swz(rr, half * 4 + k)));
+                     : "r"(sF + sQD + kTile16 + swz(rr, half * 4 + k)));
         const uint32_t w[4] = {gv.x, gv.y, gv.z, gv.w};
         const float of[8] = {ov[2 * k].x, ov[2 * k].y, ov[2 * k].z, ov[2 * k].w,
                              ov[2 * k + 1].x, ov[2 * k + 1].y, ov[2 * k + 1].z, ov[2 * k + 1].w};
@@ -2565,7 +2585,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           dsum = fmaf(__uint_as_float(w[t] & 0xffff0000u), of[2 * t + 1], dsum);
         }
       }
-      __syncwarp();  // stage 1 is overwritten by fine block 1
+      __syncwarp();  // the Q/dO stage is overwritten by fine block kFS-1
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
       const uint32_t tb = i & 1;
       if (half == 0) {
@@ -2585,24 +2605,27 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dq[j][e] = 0.f;
       for (uint32_t j = 0; j < p.K; ++j) {
-        if (j + 1 < p.K) load_fine(j + 1);
+        if (j + kFS - 1 < p.K) load_fine(j + kFS - 1);
         cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<kFS - 1>();
         __syncwarp();
-        const uint32_t base = sF + (j & 1) * 4096;
+        const uint32_t base = sF + (j % kFS) * 4096;
         attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
                          lse1, D0, D1, lane, dq);
         __syncwarp();
       }
-      // publish the fine part of dQ (unscaled) for the coarse warps' epilogue
-      if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
-      const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
+      // publish the fine part of dQ (unscaled) in TMEM (lanes 16 fw.., the
+      // mma fragment layout via tcgen05.st.16x256b) for the coarse epilogue
+      if (tid == 224) trace_ev(p, 5, i, 1);
+      if (i >= 2) mbar_wait(bar(FFREE + tb), ((i >> 1) - 1) & 1);
+      if (tid == 224) trace_ev(p, 5, i, 2);
+      fence_after();
+      const uint32_t tq = tmem + ((16u * fw) << 16) + 384 + 64 * tb;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        *reinterpret_cast<float2*>(dqs + dqf_idx(r0, j * 8 + cc)) = make_float2(dq[j][0], dq[j][1]);
-        *reinterpret_cast<float2*>(dqs + dqf_idx(r1, j * 8 + cc)) = make_float2(dq[j][2], dq[j][3]);
-      }
-      mbar_arrive(bar(FDONE));
+      for (int j = 0; j < 8; ++j) tmem_st_frag(tq + 8 * j, dq[j][0], dq[j][1], dq[j][2], dq[j][3]);
+      tmem_st_wait();
+      fence_before();
+      mbar_arrive(bar(FDONE + tb));
     }
   }
   fence_before();

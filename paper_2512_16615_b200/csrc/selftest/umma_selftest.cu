@@ -76,7 +76,43 @@ __global__ void __launch_bounds__(128) selftest_kernel(const __nv_bfloat16* a,
   if (warp == 0) tmem_dealloc(tmem, ncols);
 }
 
+// tcgen05.st.16x256b from mma-fragment registers, read back with 32x32b:
+// warp w writes lanes 32w + 16h (h = 0, 1) with value lane*100 + col.
+__global__ void __launch_bounds__(128) frag_store_kernel(float* out) {
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) tmem_alloc(llsa_tc::smem_u32(&tslot), 32);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tslot;
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t base = 32 * warp + 16 * h;
+    const int r = lane >> 2, c = 2 * (lane & 3);
+    for (int t = 0; t < 4; ++t)  // columns 8t .. 8t+7
+      tmem_st_frag(tmem + (base << 16) + 8 * t, (base + r) * 100.f + 8 * t + c,
+                   (base + r) * 100.f + 8 * t + c + 1, (base + r + 8) * 100.f + 8 * t + c,
+                   (base + r + 8) * 100.f + 8 * t + c + 1);
+  }
+  tmem_st_wait();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  uint32_t v[32];
+  tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
+  tmem_ld_wait();
+  for (int i = 0; i < 32; ++i) out[(32 * warp + lane) * 32 + i] = __uint_as_float(v[i]);
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 32);
+}
+
 }  // namespace
+
+extern "C" int llsa_umma_frag_selftest(float* out, void* stream) {
+  frag_store_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
 
 extern "C" int llsa_umma_selftest(const void* a, const void* b, float* d, int N, int a_mn,
                                   int b_mn, int b_lbo, void* stream) {

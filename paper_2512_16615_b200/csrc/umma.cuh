@@ -200,6 +200,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t& r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r) : "r"(taddr));
 }
+// 16 TMEM lanes x 8 fp32 columns in the mma.sync m16n8 accumulator layout:
+// thread t holds (row t/4, cols 2(t%4), +1) in r0, r1 and (row t/4 + 8, same
+// cols) in r2, r3.  `taddr` = (lane base << 16) | column; the lane base must
+// lie in the calling warp's sub-partition.
+__device__ __forceinline__ void tmem_st_frag(uint32_t taddr, float c0, float c1, float c2,
+                                             float c3) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x1.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr),
+               "r"(__float_as_uint(c0)), "r"(__float_as_uint(c1)), "r"(__float_as_uint(c2)),
+               "r"(__float_as_uint(c3))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }

@@ -297,3 +297,40 @@ def test_handle_path_matches_oracle(oracle_c, cfg, bf):
         assert torch.equal(out, out2)
         for a, b in zip((dq, dk, dv), g2):
             assert torch.equal(a, b)
+
+
+# ------------------------------------------- full-size tcgen05 path vs SIMT path
+# The L = 3 backward (B = 16 needs N >= 65536) is beyond what the C oracle
+# runs in test time, so the tensor-core handle path is checked against the
+# staged SIMT path (fp32 math, itself pinned to the oracle above) on the same
+# bf16 inputs: tables bit-exact, outputs and gradients within the bf16 bar.
+# K = 16 gives 33 coarse entries, past the tcgen05 forward / dQ kernels'
+# 24-entry TMEM budget, so it runs their mma.sync fallbacks.
+@pytest.mark.parametrize("cfg", [Config(65536, 64, 16, 8, 3, 3),
+                                 Config(65536, 64, 16, 16, 3, 3),
+                                 Config(65536, 64, 16, 8, 3, 1),
+                                 Config(65536, 64, 16, 8, 3, 3, reweight_mode=1)],
+                         ids=["C3", "C3-K16", "C3-Le1", "C3-LogitBias"])
+def test_full_size_tensor_core_path_matches_simt(cfg):
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v, dO = (torch.randn(1, cfg.n, 64, device="cuda", generator=g).to(torch.bfloat16)
+                   for _ in range(4))
+    lc = llsa.LLSAConfig(cfg.n, 64, 16, cfg.top_k, cfg.levels, cfg.enrich_levels,
+                         reweight_mode=cfg.reweight_mode)
+    h = llsa.LLSAHandle(lc, 1, torch.bfloat16)
+    assert h.uses_tensor_cores
+    out = h.forward(q, k, v)
+    dq, dk, dv = h.backward(dO, q, k, v, out)
+    llsa.sync_status()
+    vc = llsa.validate_config(lc)
+    pq, pk, pv = (llsa.build_pyramid(t, 16, cfg.levels) for t in (q, k, v))
+    tables = llsa.hierarchical_topk(pq, pk, vc)
+    assert torch.equal(h.view("tables").view(-1), tables.view(-1))
+    st = llsa.llsa_forward(q, k, v, pk, pv, tables, vc)
+    tr = llsa.transpose_all(tables, vc)
+    rq, rk, rv = llsa.llsa_backward(dO, st, q, k, v, pk, pv, tables, tr, vc)
+    llsa.sync_status()
+    for name, got, want in (("out", out, st.output), ("dq", dq, rq), ("dk", dk, rk),
+                            ("dv", dv, rv)):
+        e = rel_err(got[0].cpu().numpy(), want[0].cpu().numpy())
+        assert e["max_rel"] <= 2e-2, (name, e)

@@ -34,3 +34,16 @@ def test_umma_gemm(n, lbo, a_mn, b_mn):
     torch.cuda.synchronize()
     ref = A.float() @ B.float()
     assert torch.allclose(d, ref, atol=1e-3, rtol=1e-3), (d - ref).abs().max().item()
+
+
+def test_tmem_store_from_mma_fragments():
+    # tcgen05.st.16x256b writes 16 lanes x 8 columns in the m16n8 accumulator
+    # layout (the fine warps stage partial results in TMEM this way)
+    lib = C.CDLL(SO)
+    out = torch.zeros(128, 32, device="cuda")
+    assert lib.llsa_umma_frag_selftest(C.c_void_p(out.data_ptr()),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    torch.cuda.synchronize()
+    lane = torch.arange(128, device="cuda").float()[:, None]
+    col = torch.arange(32, device="cuda").float()[None, :]
+    assert torch.equal(out, lane * 100 + col)

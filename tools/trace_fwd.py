@@ -17,6 +17,8 @@ out = torch.empty(units, n, 64, device="cuda")
 lib = llsa._lib.load()
 buf = (C.c_ulonglong * 8192)()
 which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
+if which == "bwd" and len(sys.argv) > 2:
+    os.environ.update({"LLSA_KVF": "0"} if sys.argv[2] == "dq" else {})
 dO = torch.randn_like(q)
 g = [torch.empty(units, n, 64, device="cuda") for _ in range(3)]
 for it in range(2):
@@ -32,7 +34,7 @@ for idx, x in enumerate(buf[:cnt]):
     if x >> 63:
         ev.append((idx // 1024, (idx // 32) % 32, idx % 32, x & 0x7FFFFFFFFFFFFFFF))
 t0 = min(e[3] for e in ev)
-names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "epi", 6: "dKV"}
+names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "fine", 6: "dQ/dKV", 7: "c-epi"}
 ev.sort(key=lambda e: e[3])
 for r, t, e, c in ev:
     if t < 8:
