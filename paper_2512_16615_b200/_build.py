@@ -29,7 +29,7 @@ CXX = shutil.which("g++") or "g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
-                     f"-I{INCLUDE}", f"-I{CSRC}"]
+                     f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("LLSA_NVCC_EXTRA", "").split()
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", f"-I{INCLUDE}",
              "-I/usr/local/cuda/include"]
 

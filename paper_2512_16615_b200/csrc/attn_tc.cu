@@ -31,6 +31,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1374,7 +1375,7 @@ __global__ void __launch_bounds__(256, 2) tc5_dq_coarse_kernel(TcParams p) {
 // thread arrivals), so loads, MMAs and the elementwise work of consecutive
 // chunks and tiles overlap.
 struct TmaMaps {
-  CUtensorMap q, g, khi, vhi, klo, vlo;
+  CUtensorMap q, g, khi, vhi, klo, vlo, o;
 };
 
 namespace dqp {
@@ -1754,7 +1755,6 @@ constexpr int kVStage = 8192;
 constexpr int kPBytes = kTileQ * 128;           // 128 rows x 64 keys bf16
 constexpr int kFineStages = 2;
 constexpr int kQStages = 1;
-constexpr int kOfStride = 68;                   // fp32 O_f staging row stride (floats)
 constexpr int kFineWarp = kFineStages * 4096;   // per fine warp: {K, V} blocks
 constexpr int kMaxChunks = 6;
 constexpr int kOffQ = 0;
@@ -1762,19 +1762,24 @@ constexpr int kOffK = kOffQ + kQStages * kQBytes;      // 16 KB
 constexpr int kOffV = kOffK + kKRing * kKStage;        // 64 KB
 constexpr int kOffP = kOffV + kVRing * kVStage;        // 80 KB
 constexpr int kOffFine = kOffP + 2 * kPBytes;          // 112 KB
-constexpr int kOffOf = kOffFine + 8 * kFineWarp;       // 176 KB: fine partial O_f [128][68]
-constexpr int kOffStat = kOffOf + kTileQ * kOfStride * 4;
-constexpr int kOffEnt = kOffStat + 3 * kTileQ * 4;     // + (m_f, l_f, true max)
+// 176 KB: fine partial O_f, then the merged output tile, fp32 as two SW128
+// halves [128 rows][32 cols] — the TMA store box layout
+constexpr int kOffOf = kOffFine + 8 * kFineWarp;
+constexpr int kOfHalf = kTileQ * 128;
+constexpr int kOffStat = kOffOf + 2 * kOfHalf;
+constexpr int kOffEnt = kOffStat + 5 * kTileQ * 4;  // m_f, l_f, true max, pair max [2]
 // ones tile (1024-aligned: a SW128 atom): B operand column 64 of the PV MMA (l_c)
-constexpr int kOffOnes = (kOffEnt + 1024 + 1023) & ~1023;  // after bias[32], chunk info, rows[2][32]
+constexpr int kOffOnes = (kOffEnt + 1024 + 1023) & ~1023;  // after bias[32], chunk info, unit table
 constexpr int kOffBar = kOffOnes + 8192;
 enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 8, VFULL = 12, VEMPTY = 15, SREADY = 18,
        SFREE = 24, PFULL = 30, PEMPTY = 32, OREADY = 34, OFREE = 36, FDONE = 38, FFREE = 39,
        NBAR = 40 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
-constexpr int kThreads = 16 * 32;  // 0 K' gather, 1 S MMA, 2 V' gather, 3-6 coarse, 7-14 fine,
-                                   // 15 Q TMA + PV MMA
-constexpr uint32_t kTmemCols = 512;  // S: [0, 384), O: 384 + 64·buffer
+// warps: 0 K' gather, 1 S MMA, 2 V' gather, 3-10 coarse (two per TMEM lane
+// quadrant), 11-18 fine, 19 Q TMA + PV MMA
+constexpr int kCoarse0 = 3, kFine0 = 11, kQPV = 19;
+constexpr int kThreads = 20 * 32;
+constexpr uint32_t kTmemCols = 512;  // S [0, 64·nch), O_c | l_c buffers of 96
 constexpr uint32_t kMaxEntries = 4 * kMaxChunks;
 }  // namespace fw5
 
@@ -1789,7 +1794,10 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
   auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
   float* fstat = reinterpret_cast<float*>(smem + kOffStat);  // [m_f | l_f][128]
-  float* ofs = reinterpret_cast<float*>(smem + kOffOf);      // O_f [128][kOfStride]
+  // byte offset of float4 column group c4 (0..15) of row r in the O_f tile
+  auto of_off = [](uint32_t r, uint32_t c4) {
+    return (c4 >> 3) * kOfHalf + r * 128 + (((c4 & 7) ^ (r & 7)) << 4);
+  };
   const uint64_t tpu = p.n / kTileQ;
   const uint64_t total = tpu * units;
   const uint32_t nce = p.nce, nch = (nce + 3) / 4;
@@ -1805,9 +1813,21 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
   // entry, and per 64-key chunk its entry count and whether it needs K'_lo
   float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
   uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
-  uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 256);  // [K | V][32]
   if (tid < nce) ent_bias[tid] = p.bias2[entry_level(p, tid)];
   if (tid < nch) ch_info[tid] = chunk_ne(tid) | (chunk_lo(tid) ? 0x100u : 0u);
+  // coarse-warp work units: 32 TMEM columns (two entries) each, as
+  // chunk | half << 5 | last-of-chunk << 6
+  uint32_t* utab = reinterpret_cast<uint32_t*>(smem + kOffEnt + 192);
+  uint32_t nu = 0;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    const bool two = chunk_ne(ch) > 2;
+    if (tid == 0) utab[nu] = ch | (two ? 0u : 64u);
+    ++nu;
+    if (two) {
+      if (tid == 0) utab[nu] = ch | 32u | 64u;
+      ++nu;
+    }
+  }
   // a [64 keys][64] MN-major SW128 tile whose column 0 is 1.0: the second N
   // block of the PV MMA's B operand, so TMEM column 64 of O_c accumulates l_c
   for (uint32_t x = tid; x < 64 * 8; x += blockDim.x) {
@@ -1825,25 +1845,25 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(QFULL + i), 1);
       mbar_init(bar(QEMPTY + i), 1 + 256);  // S MMAs done + fine warps hold Q
-      mbar_init(bar(PFULL + i), 128);
+      mbar_init(bar(PFULL + i), 256);
       mbar_init(bar(PEMPTY + i), 1);
       mbar_init(bar(OREADY + i), 1);
-      mbar_init(bar(OFREE + i), 128);
+      mbar_init(bar(OFREE + i), 256);
     }
     for (int i = 0; i < kKRing; ++i) {
-      mbar_init(bar(KFULL + i), 1);
+      mbar_init(bar(KFULL + i), 32);  // one cp.async arrival per producer lane
       mbar_init(bar(KEMPTY + i), 1);
     }
     for (int i = 0; i < kVRing; ++i) {
-      mbar_init(bar(VFULL + i), 1);
+      mbar_init(bar(VFULL + i), 32);
       mbar_init(bar(VEMPTY + i), 1);
     }
     for (int i = 0; i < kMaxChunks; ++i) {
       mbar_init(bar(SREADY + i), 1);
-      mbar_init(bar(SFREE + i), 128);
+      mbar_init(bar(SFREE + i), 256);
     }
     mbar_init(bar(FDONE), 256);
-    mbar_init(bar(FFREE), 128);
+    mbar_init(bar(FFREE), 256);
     fence_mbar_init();
   }
   fence_before();
@@ -1853,33 +1873,34 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
 
   if (warp == 0 || warp == 2) {
     // ------------------------------------------------------------ producers
-    // warp 0: Q tile + coarse K' chunks; warp 2: coarse V' chunks.  Each
-    // resolves the tile's coarse rows itself, so the K' side runs ahead of
-    // the PV side by as many tiles as its ring allows.
+    // warp 0: coarse K' chunks; warp 2: coarse V' chunks.  Each resolves the
+    // tiles' coarse rows itself (one tile ahead), so the K' side runs ahead
+    // of the PV side by as many tiles as its ring allows.
     const bool kside = warp == 0;
     // The coarse rows are gathered with cp.async by all 32 lanes (16 B per
     // lane per instruction; a 2 KB entry is 4 per lane) into the 128-byte
-    // swizzled layout the UMMA descriptors expect; a chunk is published
-    // (proxy fence + FULL arrive) once the lanes' copies of it have landed,
-    // one chunk behind the issue front.  Per-entry TMA boxes were issue-bound
-    // here (~150 cycles per 2 KB box).
+    // swizzled layout the UMMA descriptors expect; each lane's copies of a
+    // chunk arrive on the chunk's FULL barrier as they land (count 32), and
+    // the consuming MMA thread fences the async proxy.  Per-entry TMA boxes
+    // were issue-bound here (~150 cycles per 2 KB box).
     const uint32_t ring = kside ? kKRing : kVRing;
     const Block16Lane bl = block16_lane(lane);
-    uint32_t* rows = ent_rows + (kside ? 0 : 32);
     const bf16* arr0 = kside ? p.khi : p.vhi;
     const bf16* arr1 = p.klo;
+    auto entry_row = [&](uint64_t id) -> uint32_t {
+      if (id >= total || lane >= nce) return 0u;
+      const uint32_t unit = (uint32_t)(id / tpu);
+      uint32_t l, r;
+      coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, (id % tpu) * kTileQ / kBS,
+                   lane, l, r);
+      return (uint32_t)(unit * p.pyr_rows) + r;
+    };
+    uint32_t rows_next = entry_row(blockIdx.x);
     uint32_t rc = 0, i = 0;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-      const uint32_t unit = (uint32_t)(id / tpu);
-      const uint64_t q0 = (id % tpu) * kTileQ;
-      if (lane < nce) {
-        uint32_t l, r;
-        coarse_entry(p, p.tables + (uint64_t)unit * p.table_entries, q0 / kBS, lane, l, r);
-        rows[lane] = (uint32_t)(unit * p.pyr_rows) + r;
-      }
-      __syncwarp();
+      const uint32_t myrow = rows_next;
+      rows_next = entry_row(id + gridDim.x);
       if (lane == 0) trace_ev(p, kside ? 1 : 2, i, 0);
-      uint32_t prev_full = 0;
       for (uint32_t ch = 0; ch < nch; ++ch, ++rc) {
         const uint32_t s = rc % ring;
         const uint32_t info = ch_info[ch], ne = info & 0xFF;
@@ -1887,24 +1908,13 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         if (rc >= ring) mbar_wait(bar((kside ? KEMPTY : VEMPTY) + s), ((rc / ring) - 1) & 1);
         const uint32_t dst = sbase + (kside ? kOffK + s * kKStage : kOffV + s * kVStage);
         for (uint32_t e = 0; e < ne; ++e) {
-          const uint64_t row = rows[ch * 4 + e];
+          const uint64_t row = __shfl_sync(0xffffffffu, myrow, ch * 4 + e);
           load_block16_async(dst + e * 2048, arr0 + row * kD, bl, lane);
           if (lo) load_block16_async(dst + 8192 + e * 2048, arr1 + row * kD, bl, lane);
         }
-        cp_async_commit();
-        if (prev_full) {
-          cp_async_wait<1>();
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(prev_full);
-        }
-        prev_full = bar((kside ? KFULL : VFULL) + s);
+        cp_async_mbar_arrive(bar((kside ? KFULL : VFULL) + s));
         if (lane == 0) trace_ev(p, kside ? 1 : 2, i, 1 + ch);
       }
-      cp_async_wait<0>();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0 && prev_full) mbar_arrive(prev_full);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -1920,6 +1930,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           const uint32_t s = kc % kKRing;
           mbar_wait(bar(KFULL + s), (kc / kKRing) & 1);
           if (i >= 1) mbar_wait(bar(SFREE + ch), (i - 1) & 1);
+          fence_proxy_async();  // the K' chunk was written by cp.async
           fence_after();
           const uint32_t ne = ch_info[ch] & 0xFF;
           const bool lo = ch_info[ch] & 0x100u;
@@ -1939,7 +1950,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         commit(bar(QEMPTY + qs));
       }
     }
-  } else if (warp == 15) {
+  } else if (warp == kQPV) {
     // ------------------------------------------------------------ Q TMA + PV issuer
     // A second MMA-issuing thread, so the S chunks of tile i+1 do not wait
     // behind tile i's PV chunks.  It also streams the Q tiles: Q(i+1) goes
@@ -1957,17 +1968,19 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       const uint32_t idesc_o = idesc_bf16(128, kD + 16, false, true);  // O | l_c
       uint32_t vc = 0, pc = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-        const uint32_t ob = i % nob;
+
         if (id + gridDim.x < total) {
           mbar_wait(bar(QEMPTY), i & 1);  // S MMAs of tile i done, fine warps hold Q
           load_q(id + gridDim.x);
         }
+        const uint32_t ob = i % nob;
         if (i >= nob) mbar_wait(bar(OFREE + ob), ((i / nob) - 1) & 1);
         const uint32_t tO = tmem + o_base + o_stride * ob;
         for (uint32_t ch = 0; ch < nch; ++ch, ++vc, ++pc) {
           const uint32_t s = vc % kVRing, ps = pc & 1;
           mbar_wait(bar(VFULL + s), (vc / kVRing) & 1);
           mbar_wait(bar(PFULL + ps), (pc >> 1) & 1);
+          fence_proxy_async();  // the V' chunk was written by cp.async
           fence_after();
           const uint32_t ne = chunk_ne(ch);
           const uint32_t sp = sbase + kOffP + ps * kPBytes;
@@ -1983,72 +1996,83 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         commit(bar(OREADY + ob));
       }
     }
-  } else if (warp >= 3 && warp < 7) {
+  } else if (warp >= kCoarse0 && warp < kCoarse0 + 8) {
     // ------------------------------------------------------------ coarse warps
-    const uint32_t row = 32 * (warp & 3) + lane;
-    const uint32_t lane_off = (32u * (warp & 3)) << 16;
+    // Two warps per TMEM lane quadrant (= per SM sub-partition) split every
+    // 64-column chunk: half h = 0 takes entries 0, 1 (columns 0-31), h = 1
+    // entries 2, 3.  The row max is exchanged through smem once per tile
+    // (named barrier per pair), so P, O_c and l_c share one exact reference.
+    const uint32_t quad = warp & 3, h = (warp - kCoarse0) >> 2;
+    const uint32_t row = 32 * quad + lane;
+    const uint32_t lane_off = (32u * quad) << 16;
+    const uint32_t pair_bar = 1 + quad;
     const float c2 = p.scale * kLog2e;
+    const uint32_t crole = warp == kCoarse0 ? 4 : warp == kCoarse0 + 4 ? 6 : 7;  // trace
+    float* pmax = reinterpret_cast<float*>(smem + kOffStat + 3 * kTileQ * 4);  // [2][128]
     uint32_t pc = 0, i = 0;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint64_t q0 = (id % tpu) * kTileQ;
-      // pass 1: row max of s·c + b over the coarse set
+      // pass 1: row max of s·c + b over this half of the coarse set
       float mx = -INFINITY;
       for (uint32_t ch = 0; ch < nch; ++ch) {
         const uint32_t ne = chunk_ne(ch);
         mbar_wait(bar(SREADY + ch), i & 1);
         fence_after();
+        if (2 * h < ne) {
+          uint32_t sv[32];
+          tmem_ld32(tmem + lane_off + 64 * ch + 32 * h, sv);
+          tmem_ld_wait();
+          const uint32_t ne_u = min(2u, ne - 2 * h);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if (2 * hh < (int)ne) {
-            uint32_t sv[32];
-            tmem_ld32(tmem + lane_off + 64 * ch + 32 * hh, sv);
-            tmem_ld_wait();
+          for (int e2 = 0; e2 < 2; ++e2) {
+            if (e2 < (int)ne_u) {
+              const uint32_t* se = sv + e2 * 16;
+              float t[8];
 #pragma unroll
-            for (int ee = 0; ee < 2; ++ee) {
-              const uint32_t e = 2 * hh + ee;
-              if (e < ne) {
-                const float bias = ent_bias[ch * 4 + e];
-                float x = __uint_as_float(sv[ee * 16]);
+              for (int k = 0; k < 8; ++k)
+                t[k] = fmaxf(__uint_as_float(se[k]), __uint_as_float(se[k + 8]));
 #pragma unroll
-                for (int k = 1; k < 16; ++k) x = fmaxf(x, __uint_as_float(sv[ee * 16 + k]));
-                mx = fmaxf(mx, fmaf(x, c2, bias));  // c > 0: max(s)·c + b = max(s·c + b)
-              }
+              for (int k = 0; k < 4; ++k) t[k] = fmaxf(t[k], t[k + 4]);
+              const float x = fmaxf(fmaxf(t[0], t[2]), fmaxf(t[1], t[3]));
+              mx = fmaxf(mx, fmaf(x, c2, ent_bias[ch * 4 + 2 * h + e2]));  // c > 0
             }
           }
         }
       }
-      if (tid == 96) trace_ev(p, 4, i, 0);
-      // pass 2: P = exp2(s·c + b − m_c) → bf16 ring; l_c
+      pmax[h * kTileQ + row] = mx;
+      named_bar_sync(pair_bar, 64);
+      mx = fmaxf(mx, pmax[(h ^ 1) * kTileQ + row]);
+      if (lane == 0) trace_ev(p, crole, i, 0);
+      // pass 2: P = exp2(s·c + b − m_c) → bf16 ring (this half's columns)
       for (uint32_t ch = 0; ch < nch; ++ch, ++pc) {
-        const uint32_t ne = chunk_ne(ch), ps = pc & 1;
+        const uint32_t ps = pc & 1;
+        const bool has = 2 * h < chunk_ne(ch);
+        uint32_t sv[32];
+        if (has) tmem_ld32(tmem + lane_off + 64 * ch + 32 * h, sv);
         if (pc >= 2) mbar_wait(bar(PEMPTY + ps), ((pc >> 1) - 1) & 1);
         const uint32_t sp = sbase + kOffP + ps * kPBytes;
+        tmem_ld_wait();
+        if (has) {
+          const uint32_t ne_u = min(2u, chunk_ne(ch) - 2 * h);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if (2 * hh < (int)ne) {
-            uint32_t sv[32];
-            tmem_ld32(tmem + lane_off + 64 * ch + 32 * hh, sv);
-            tmem_ld_wait();
+          for (int e2 = 0; e2 < 2; ++e2) {
+            if (e2 < (int)ne_u) {
+              const uint32_t e = 2 * h + e2;
+              const float nb = ent_bias[ch * 4 + e] - mx;
 #pragma unroll
-            for (int ee = 0; ee < 2; ++ee) {
-              const uint32_t e = 2 * hh + ee;
-              if (e < ne) {
-                const float nb = ent_bias[ch * 4 + e] - mx;
+              for (int half = 0; half < 2; ++half) {
+                uint32_t pk[4];
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                  uint32_t pk[4];
-#pragma unroll
-                  for (int k = 0; k < 4; ++k) {
-                    const int i0 = ee * 16 + half * 8 + k * 2;
-                    const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
-                    const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
-                    pk[k] = pack_bf16(p0, p1);
-                  }
-                  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
-                                   sp + swz(row, e * 2 + half)),
-                               "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
+                for (int k = 0; k < 4; ++k) {
+                  const int i0 = e2 * 16 + half * 8 + k * 2;
+                  const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
+                  const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
+                  pk[k] = pack_bf16(p0, p1);
                 }
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                                 sp + swz(row, e * 2 + half)),
+                             "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]));
               }
             }
           }
@@ -2057,18 +2081,21 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         mbar_arrive(bar(SFREE + ch));
         fence_proxy_async();
         mbar_arrive(bar(PFULL + ps));
+        if (lane == 0) trace_ev(p, crole, i, 24 + ch);
       }
-      // epilogue: merge with the fine partition of the same rows (staged in
-      // smem by the fine warps), O = (O_c 2^(m_c-m) + O_f 2^(m_f-m)) / l
+      // epilogue: merge this half of the columns with the fine partition of
+      // the same rows (staged in smem by the fine warps),
+      // O = (O_c 2^(m_c-m) + O_f 2^(m_f-m)) / l, then a TMA store of the box
       const uint32_t ob = i % nob;
-      if (tid == 96) trace_ev(p, 4, i, 1);
+      if (lane == 0) trace_ev(p, crole, i, 1);
       mbar_wait(bar(OREADY + ob), (i / nob) & 1);
       mbar_wait(bar(FDONE), i & 1);
-      if (tid == 96) trace_ev(p, 4, i, 2);
+      if (lane == 0) trace_ev(p, crole, i, 2);
       fence_after();
       const uint32_t tO = tmem + lane_off + o_base + o_stride * ob;
-      uint32_t lraw;
+      uint32_t lraw, ov[32];
       tmem_ld1(tO + kD, lraw);
+      tmem_ld32(tO + 32 * h, ov);
       tmem_ld_wait();
       const float lsum = __uint_as_float(lraw);
       const float mf = fstat[row], lf = fstat[kTileQ + row];
@@ -2078,38 +2105,45 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       const float inv = 1.f / lt;
       const float sc = ac * inv, sf = af * inv;
       const uint64_t ro = (uint64_t)unit * p.n + q0 + row;
-      float* o = p.out + ro * kD;
-      const float* of = ofs + row * kOfStride;
       bool bad = !(lt > 0.f) || !isfinite(lt);
+      // the merged half row overwrites its O_f half row in place; the warp
+      // then stores its 32 rows with one TMA box (coalesced, asynchronous)
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t ov[32];
-        tmem_ld32(tO + 32 * hh, ov);
-        tmem_ld_wait();
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 f = *reinterpret_cast<const float4*>(of + 32 * hh + 4 * k);
-          float4 v;
-          v.x = __uint_as_float(ov[4 * k]) * sc + f.x * sf;
-          v.y = __uint_as_float(ov[4 * k + 1]) * sc + f.y * sf;
-          v.z = __uint_as_float(ov[4 * k + 2]) * sc + f.z * sf;
-          v.w = __uint_as_float(ov[4 * k + 3]) * sc + f.w * sf;
-          bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
-          reinterpret_cast<float4*>(o + 32 * hh)[k] = v;
-        }
+      for (int k = 0; k < 8; ++k) {
+        float4* a = reinterpret_cast<float4*>(smem + kOffOf + of_off(row, 8 * h + k));
+        const float4 f = *a;
+        float4 v;
+        v.x = __uint_as_float(ov[4 * k]) * sc + f.x * sf;
+        v.y = __uint_as_float(ov[4 * k + 1]) * sc + f.y * sf;
+        v.z = __uint_as_float(ov[4 * k + 2]) * sc + f.z * sf;
+        v.w = __uint_as_float(ov[4 * k + 3]) * sc + f.w * sf;
+        bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
+        *a = v;
       }
       fence_before();
       mbar_arrive(bar(OFREE + ob));
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        const int y = (int)((uint64_t)unit * p.n + q0 + 32 * quad);
+        tma_store_2d(&m.o, sbase + kOffOf + h * kOfHalf + 32 * quad * 128, 32 * h, y);
+        bulk_commit();
+        bulk_wait_read();
+      }
+      __syncwarp();
       mbar_arrive(bar(FFREE));
-      p.row_max[ro] = mrow / kLog2e;
-      p.row_denom[ro] = lt;
+      if (h == 0) {
+        p.row_max[ro] = mrow / kLog2e;
+        p.row_denom[ro] = lt;
+      }
       if (__any_sync(0xffffffffu, bad) && lane == 0) raise_flag(p.flag, llsa_dev::kErrNonFinite);
-      if (tid == 96) trace_ev(p, 4, i, 3);
+      if (lane == 0) trace_ev(p, crole, i, 3);
     }
+    if (lane == 0) bulk_wait_all();  // output stores complete before exit
   } else {
     // ------------------------------------------------------------ fine warps
     const float c2 = p.scale * kLog2e;
-    const uint32_t fw = warp - 7;  // fine query block of the tile
+    const uint32_t fw = warp - kFine0;  // fine query block of the tile
     const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
     const uint64_t nfb = p.n / kBS;
     const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
@@ -2155,9 +2189,9 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       for (int e = 0; e < 4; ++e) st.lo[e] = 0.f;
       st.m[0] = st.m[1] = st.mt[0] = st.mt[1] = -INFINITY;
       uint32_t qf[4][4];
-      if (tid == 224) trace_ev(p, 5, i, 0);
+      if (tid == kFine0 * 32) trace_ev(p, 5, i, 0);
       mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
-      if (tid == 224) trace_ev(p, 5, i, 3);
+      if (tid == kFine0 * 32) trace_ev(p, 5, i, 3);
       const uint32_t sq = sbase + kOffQ + qs * kQBytes;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) lda(sq, fw * 16, ks, lane, qf[ks]);
@@ -2173,20 +2207,21 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         __syncwarp();
       }
       // publish the fine partition (raw O_f, m_f, l_f) for the coarse warps
-      if (tid == 224) trace_ev(p, 5, i, 1);
+      if (tid == kFine0 * 32) trace_ev(p, 5, i, 1);
       if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
-      if (tid == 224) trace_ev(p, 5, i, 2);
+      if (tid == kFine0 * 32) trace_ev(p, 5, i, 2);
       {
         // l of rows r, r + 8 sits in column 0 of the l accumulator (lane & 3 == 0)
         const float lf0 = __shfl_sync(0xffffffffu, st.lo[0], lane & ~3u);
         const float lf1 = __shfl_sync(0xffffffffu, st.lo[2], lane & ~3u);
         const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
-        float* o0 = ofs + r0 * kOfStride;
-        float* o1 = ofs + r1 * kOfStride;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          *reinterpret_cast<float2*>(o0 + j * 8 + cc) = make_float2(st.o[j][0], st.o[j][1]);
-          *reinterpret_cast<float2*>(o1 + j * 8 + cc) = make_float2(st.o[j][2], st.o[j][3]);
+          const uint32_t c4 = 2 * j + (cc >> 2), w = (cc & 3) * 4;
+          *reinterpret_cast<float2*>(smem + kOffOf + of_off(r0, c4) + w) =
+              make_float2(st.o[j][0], st.o[j][1]);
+          *reinterpret_cast<float2*>(smem + kOffOf + of_off(r1, c4) + w) =
+              make_float2(st.o[j][2], st.o[j][3]);
         }
         if ((lane & 3) == 0) {
           fstat[r0] = st.m[0];
@@ -2536,8 +2571,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           b = 0;
         }
         const uint32_t base = sF + (j % kFS) * 4096;
-        load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
-        load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        if (!(p.dbg & 16)) {
+          load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
+          load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        }
       };
       // blocks 0 .. kFS-2 prefetched; this warp's own 16 Q and dO rows go to
       // the last ring stage (free until block kFS-1 is loaded)
@@ -2610,7 +2647,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         cp_async_wait<kFS - 1>();
         __syncwarp();
         const uint32_t base = sF + (j % kFS) * 4096;
-        attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
+        if (!(p.dbg & 8)) attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
                          lse1, D0, D1, lane, dq);
         __syncwarp();
       }
@@ -3455,11 +3492,13 @@ void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out) {
 
 // 2-D TMA map over a [rows][64] bf16 tensor, boxes of box_rows × 64,
 // 128-byte swizzle (the K-major / MN-major SW128 operand layout).
+// With f32 = true: a [rows][64] fp32 tensor, boxes of box_rows × 32 (the
+// output tile store).
 static llsa_status make_tma_map(CUtensorMap* map, const void* base, uint64_t rows,
-                                uint32_t box_rows) {
+                                uint32_t box_rows, bool f32 = false) {
   const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kD, box_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kD * (f32 ? 4 : 2)};
+  const cuuint32_t box[2] = {(cuuint32_t)(f32 ? 32 : kD), box_rows};
   const cuuint32_t estr[2] = {1, 1};
   // resolved through the runtime so the library has no link-time libcuda
   // dependency (it must load on hosts without a driver)
@@ -3478,7 +3517,8 @@ static llsa_status make_tma_map(CUtensorMap* map, const void* base, uint64_t row
     encode = reinterpret_cast<EncodeFn>(fn);
   }
   const CUresult r = encode(
-      map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+      map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+      const_cast<void*>(base), dims, strides, box,
       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(LLSA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -3545,6 +3585,7 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
     if (llsa_status st = make_tma_map(&maps.khi, tb.k_hi, pyr_rows, kBS)) return st;
     if (llsa_status st = make_tma_map(&maps.klo, tb.k_lo, pyr_rows, kBS)) return st;
     if (llsa_status st = make_tma_map(&maps.vhi, tb.v_hi, pyr_rows, kBS)) return st;
+    if (llsa_status st = make_tma_map(&maps.o, out, in_rows, 32, true)) return st;
     const uint64_t tiles = (g.n / kTileQ) * units;
     const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
     tc5_fwd_kernel<<<grid, fw5::kThreads, fw5::kSmem, s>>>(P, maps, units);

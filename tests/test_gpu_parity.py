@@ -334,3 +334,4 @@ def test_full_size_tensor_core_path_matches_simt(cfg):
                             ("dv", dv, rv)):
         e = rel_err(got[0].cpu().numpy(), want[0].cpu().numpy())
         assert e["max_rel"] <= 2e-2, (name, e)
+

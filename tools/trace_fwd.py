@@ -22,10 +22,12 @@ if which == "bwd" and len(sys.argv) > 2:
 dO = torch.randn_like(q)
 g = [torch.empty(units, n, 64, device="cuda") for _ in range(3)]
 for it in range(2):
+    if which == "fwd":
+        lib.llsa_debug_trace(buf, 8192)  # reset
     h.forward(q, k, v, out)
     torch.cuda.synchronize()
-    lib.llsa_debug_trace(buf, 8192)  # reset
     if which == "bwd":
+        lib.llsa_debug_trace(buf, 8192)  # reset
         h.backward(dO, q, k, v, out, *g)
         torch.cuda.synchronize()
 cnt = lib.llsa_debug_trace(buf, 8192)
@@ -34,7 +36,7 @@ for idx, x in enumerate(buf[:cnt]):
     if x >> 63:
         ev.append((idx // 1024, (idx // 32) % 32, idx % 32, x & 0x7FFFFFFFFFFFFFFF))
 t0 = min(e[3] for e in ev)
-names = {1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "fine", 6: "dQ/dKV", 7: "c-epi"}
+names = {0: "coars6", 1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine", 6: "coars4", 7: "coars5"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "fine", 6: "dQ/dKV", 7: "c-epi"}
 ev.sort(key=lambda e: e[3])
 for r, t, e, c in ev:
     if t < 8:
