@@ -2700,11 +2700,14 @@ constexpr int kStage = 38912;                  // 38 KB, 1024-aligned
 constexpr int kRing = 4;
 constexpr int kOffB = kRing * kStage;          // 152 KB: B' x 2 (16 KB each)
 constexpr int kOffInfo = kOffB + 2 * 16384;    // per-stage chunk facts
-constexpr int kOffBar = kOffInfo + 64;
+constexpr int kFactSlots = 8, kFactWords = 36;  // item facts ring: lo, hi, ids[32]
+constexpr int kOffFacts = kOffInfo + 64;
+constexpr int kOffBar = kOffFacts + kFactSlots * kFactWords * 4;
 enum { FULL = 0, EMPTY = 4, SREADY = 8, SFREE = 10, BREADY = 12, BFREE = 14, AREADY = 16,
-       AFREE = 18, NBAR = 20 };
+       AFREE = 18, FACTF = 20, FACTE = 28, NBAR = 36 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
-constexpr int kThreads = 14 * 32;    // gather 0, 2, 11, 12; MMA 1, 13; softmax 3-6; epilogue 7-10
+// gather 0, 2, 11, 12; MMA 1, 13; softmax 3-6; epilogue 7-10; item facts 14
+constexpr int kThreads = 15 * 32;
 constexpr uint32_t kTmemCols = 256;  // S|dP x 2 at [0, 64), Acc x 2 at 64, 128
 }  // namespace kvf
 
@@ -2740,6 +2743,10 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       mbar_init(bar(AREADY + i), 1);
       mbar_init(bar(AFREE + i), 128);
     }
+    for (int i = 0; i < kFactSlots; ++i) {
+      mbar_init(bar(FACTF + i), 1);
+      mbar_init(bar(FACTE + i), 4);  // the four gather warps
+    }
     fence_mbar_init();
   }
   fence_before();
@@ -2766,31 +2773,20 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     const uint32_t gi = warp == 0 ? 0u : warp == 2 ? 1u : warp - 9;
     const Block16Lane bl = block16_lane(lane);
     const uint64_t nqb = p.n / kBS;
-    // Item facts are software-pipelined so no dependent global load sits on
-    // the issue path: the CSC offsets of item i+2 and the first 32 query-block
-    // ids of item i+1 are in flight while item i is issued.
-    const uint32_t* off0 = p.csc_off + p.csc_off_off[0];
+    // Item facts (CSC segment bounds, first 32 query-block ids) come from the
+    // facts warp through a smem ring filled up to 8 items ahead, so no
+    // dependent global load sits on the issue path.
     const uint32_t* flat0 = p.csc_flat + p.csc_flat_off[0];
-    auto offs = [&](uint64_t id, uint32_t& lo, uint32_t& hi) {
-      lo = hi = 0;
-      if (id >= total) return;
-      const uint32_t* o = off0 + (id / nkb) * p.csc_off_entries + id % nkb;
-      lo = o[0];
-      hi = o[1];
-    };
-    auto ids = [&](uint64_t id, uint32_t lo, uint32_t hi) -> uint32_t {
-      return id < total && lo + lane < hi ? flat0[(id / nkb) * p.csc_flat_entries + lo + lane]
-                                          : 0u;
-    };
+    const uint32_t* fact = reinterpret_cast<const uint32_t*>(smem + kOffFacts);
     const uint64_t G = gridDim.x;
-    uint32_t lo0, hi0, lo1, hi1, lo2, hi2;
-    offs(blockIdx.x, lo0, hi0);
-    offs(blockIdx.x + G, lo1, hi1);
-    uint32_t ids0 = ids(blockIdx.x, lo0, hi0);
-    uint32_t ids1 = ids(blockIdx.x + G, lo1, hi1);
-    uint32_t rc = 0;
-    for (uint64_t id = blockIdx.x; id < total; id += G) {
-      offs(id + 2 * G, lo2, hi2);
+    uint32_t rc = 0, it = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+      const uint32_t fs = it % kFactSlots;
+      mbar_wait(bar(FACTF + fs), (it / kFactSlots) & 1);
+      const uint32_t lo0 = fact[fs * kFactWords], hi0 = fact[fs * kFactWords + 1];
+      const uint32_t ids0 = fact[fs * kFactWords + 4 + lane];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(FACTE + fs));
       const uint32_t unit = (uint32_t)(id / nkb);
       const uint64_t kb = id % nkb;
       const uint32_t m = hi0 - lo0;
@@ -2830,12 +2826,6 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         cp_async_mbar_arrive(bar(FULL + s));
         if (gi == 0 && lane == 0) trace_ev(p, 1, rc, 2);
       }
-      lo0 = lo1;
-      hi0 = hi1;
-      ids0 = ids1;
-      lo1 = lo2;
-      hi1 = hi2;
-      ids1 = ids(id + 2 * G, lo1, hi1);
     }
     // terminal marker
     {
@@ -2844,6 +2834,51 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       if (gi == 0 && lane == 0) info[s] = 0x400u;
       __syncwarp();
       mbar_arrive(bar(FULL + s));
+    }
+  } else if (warp == 14) {
+    // ------------------------------------------------------------ item facts
+    // batches of kFactSlots items: lane j loads the segment bounds of item
+    // k + j, then every item's first 32 query-block ids load in parallel
+    const uint32_t* off0 = p.csc_off + p.csc_off_off[0];
+    const uint32_t* flat0 = p.csc_flat + p.csc_flat_off[0];
+    uint32_t* fact = reinterpret_cast<uint32_t*>(smem + kOffFacts);
+    const uint64_t G = gridDim.x;
+    for (uint32_t k0 = 0;; k0 += kFactSlots) {
+      const uint64_t id0 = blockIdx.x + (uint64_t)k0 * G;
+      if (id0 >= total) break;
+      uint32_t lo = 0, hi = 0;
+      {
+        const uint64_t id = id0 + (uint64_t)lane * G;
+        if (lane < (uint32_t)kFactSlots && id < total) {
+          const uint32_t* o =
+              off0 + (uint64_t)(id / nkb) * p.csc_off_entries + id % nkb;
+          lo = o[0];
+          hi = o[1];
+        }
+      }
+      uint32_t qb[kFactSlots];
+#pragma unroll
+      for (int j = 0; j < kFactSlots; ++j) {
+        const uint64_t id = id0 + (uint64_t)j * G;
+        const uint32_t l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
+        qb[j] = id < total && l + lane < h
+                    ? flat0[(uint64_t)(id / nkb) * p.csc_flat_entries + l + lane]
+                    : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kFactSlots; ++j) {
+        const uint32_t it = k0 + j;
+        if (id0 + (uint64_t)j * G >= total) break;
+        const uint32_t l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
+        if (it >= (uint32_t)kFactSlots) mbar_wait(bar(FACTE + j), ((it / kFactSlots) - 1) & 1);
+        if (lane == 0) {
+          fact[j * kFactWords] = l;
+          fact[j * kFactWords + 1] = h;
+        }
+        fact[j * kFactWords + 4 + lane] = qb[j];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(FACTF + j));
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ S / dP issuer
@@ -2962,34 +2997,41 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     const bool is_v = qd >= 2;                     // rows 64-127: dO^T → dV
     const uint32_t dcol = lane + 32 * (qd & 1);    // head-dim column
     const uint32_t lane_off = (32u * qd) << 16;
-    // per item: segment length and the sum of the coarse pooled-adjoint rows
-    // for this column (B = 16 here: level-l row of token t is t >> 4l),
-    // fetched two items ahead
-    auto facts = [&](uint64_t id, uint32_t& m, float& add) {
-      m = 0;
-      add = 0.f;
+    // per item: segment length and the coarse pooled-adjoint rows for this
+    // column (B = 16 here: level-l row of token t is t >> 4l), loaded three
+    // items ahead into one of four register sets (the loop is unrolled by
+    // four so no loaded value is touched before its item)
+    constexpr int kEL = 4;  // coarse level slots on this path (L <= 4)
+    struct EpiFacts {
+      uint32_t o0, o1;
+      float v[kEL];
+    };
+    auto issue = [&](uint64_t id, EpiFacts& f) {
+      f.o0 = f.o1 = 0;
+#pragma unroll
+      for (int sl = 0; sl < kEL; ++sl) f.v[sl] = 0.f;
       if (id >= total) return;
       const uint32_t unit = (uint32_t)(id / nkb);
       const uint64_t kb = id % nkb;
       const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[0];
-      m = off[kb + 1] - off[kb];
-      for (uint32_t sl = 0; sl < p.ncl; ++sl) {
-        const uint32_t l = p.cl_level[sl];
-        const float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
-        const float* src = is_v ? gk + (uint64_t)p.cl_split[sl] * (p.n >> (4 * l)) * kD : gk;
-        add += src[((kb * kBS) >> (4 * l)) * kD + dcol];
+      f.o0 = off[kb];
+      f.o1 = off[kb + 1];
+#pragma unroll
+      for (int sl = 0; sl < kEL; ++sl) {
+        if (sl < (int)p.ncl) {
+          const uint32_t l = p.cl_level[sl];
+          const float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
+          const float* src = is_v ? gk + (uint64_t)p.cl_split[sl] * (p.n >> (4 * l)) * kD : gk;
+          f.v[sl] = src[((kb * kBS) >> (4 * l)) * kD + dcol];
+        }
       }
     };
-    uint32_t ai = 0, m1, m2;
-    float add1, add2;
-    facts(blockIdx.x, m1, add1);
-    facts(blockIdx.x + gridDim.x, m2, add2);
-    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x) {
-      const uint32_t m = m1;
-      const float add = add1;
-      m1 = m2;
-      add1 = add2;
-      facts(id + 2 * gridDim.x, m2, add2);
+    uint32_t ai = 0;
+    auto body = [&](uint64_t id, const EpiFacts& f) {
+      const uint32_t m = f.o1 - f.o0;
+      float add = 0.f;
+#pragma unroll
+      for (int sl = 0; sl < kEL; ++sl) add += f.v[sl];
       const uint32_t unit = (uint32_t)(id / nkb);
       const uint64_t kb = id % nkb;
       float acc[16];
@@ -3014,6 +3056,24 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       float* dst = (is_v ? p.dv : p.dk) + ((uint64_t)unit * p.n + kb * kBS) * kD + dcol;
 #pragma unroll
       for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
+    };
+    const uint64_t G = gridDim.x;
+    EpiFacts fa, fb, fc, fd;
+    issue(blockIdx.x, fa);
+    issue(blockIdx.x + G, fb);
+    issue(blockIdx.x + 2 * G, fc);
+    for (uint64_t id = blockIdx.x; id < total; id += 4 * G) {
+      issue(id + 3 * G, fd);
+      body(id, fa);
+      if (id + G >= total) break;
+      issue(id + 4 * G, fa);
+      body(id + G, fb);
+      if (id + 2 * G >= total) break;
+      issue(id + 5 * G, fb);
+      body(id + 2 * G, fc);
+      if (id + 3 * G >= total) break;
+      issue(id + 6 * G, fc);
+      body(id + 3 * G, fd);
     }
   }
   fence_before();
@@ -3373,7 +3433,8 @@ bool fwd5_path(const Geometry& g) {
 bool kvf_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   const char* f = getenv("LLSA_KVF");
-  return !(e && e[0] == '1') && !(f && f[0] == '0');
+  // the epilogue holds at most 4 coarse level slots per item (ncl <= L)
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && g.L <= 4;
 }
 
 // fused tcgen05 dq: coarse chunks of <= 4 entries, K <= 32 fine blocks per row

@@ -39,5 +39,5 @@ t0 = min(e[3] for e in ev)
 names = {0: "coars6", 1: "Kprod", 2: "Vprod", 3: "MMA", 4: "coarse", 5: "fine", 6: "coars4", 7: "coars5"} if which == "fwd" else {1: "prod", 3: "S", 4: "softmax", 5: "fine", 6: "dQ/dKV", 7: "c-epi"}
 ev.sort(key=lambda e: e[3])
 for r, t, e, c in ev:
-    if t < 8:
+    if t < int(os.environ.get("TRACE_TMAX", "8")):
         print(f"{c - t0:>9} {names.get(r, r):>6} tile {t:3d} ev {e}")
