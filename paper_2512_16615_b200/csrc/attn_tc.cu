@@ -2686,7 +2686,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
 // pooled adjoint (already reduced) and writes dk, dv once.
 // Replaces P/src/attention_grad.cpp:43-73,127-135 (+ :149-161,184-196).
 //   warps 0,2,11,12  cp.async gather (Q, dO rows of the segment; K, V of kb;
-//                    lse, D) → 4-stage ring, completion via
+//                    lse, D) → 5-stage ring, completion via
 //                    cp.async.mbarrier.arrive; chunk facts in smem
 //   warp 1 (1 ln)    S / dP issuer;  warp 13 (1 ln)  accumulate issuer
 //   warps 3-6        softmax, thread = gathered query (TMEM lane)
@@ -2697,14 +2697,15 @@ namespace kvf {
 constexpr int kQOff = 0, kGOff = 16384, kKOff = 32768, kVOff = 34816, kLseOff = 36864,
               kDOff = 37376;
 constexpr int kStage = 38912;                  // 38 KB, 1024-aligned
-constexpr int kRing = 4;
-constexpr int kOffB = kRing * kStage;          // 152 KB: B' x 2 (16 KB each)
+constexpr int kRing = 5;
+constexpr int kOffB = kRing * kStage;          // 190 KB: B' x 2 (16 KB each)
 constexpr int kOffInfo = kOffB + 2 * 16384;    // per-stage chunk facts
 constexpr int kFactSlots = 8, kFactWords = 36;  // item facts ring: lo, hi, ids[32]
 constexpr int kOffFacts = kOffInfo + 64;
 constexpr int kOffBar = kOffFacts + kFactSlots * kFactWords * 4;
-enum { FULL = 0, EMPTY = 4, SREADY = 8, SFREE = 10, BREADY = 12, BFREE = 14, AREADY = 16,
-       AFREE = 18, FACTF = 20, FACTE = 28, NBAR = 36 };
+enum { FULL = 0, EMPTY = kRing, SREADY = 2 * kRing, SFREE = SREADY + 2, BREADY = SFREE + 2,
+       BFREE = BREADY + 2, AREADY = BFREE + 2, AFREE = AREADY + 2, FACTF = AFREE + 2,
+       FACTE = FACTF + kFactSlots, NBAR = FACTE + kFactSlots };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
 // gather 0, 2, 11, 12; MMA 1, 13; softmax 3-6; epilogue 7-10; item facts 14
 constexpr int kThreads = 15 * 32;
