@@ -3204,19 +3204,20 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       uint32_t unit, slice, group;
       uint64_t row;
       decode(id, unit, row, slice, group);
-      uint32_t b = p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K +
-                            group * 8 + lane];
-      if (b >= nblk) {
-        raise_flag(p.flag, llsa_dev::kErrIndex);
-        b = 0;
-      }
-      return b;
+      return p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K +
+                      group * 8 + lane];
     };
+    // ids of item i+1 load while item i is issued; range-checked at use so
+    // the load is not waited for early
     uint32_t ids_next = key_ids(blockIdx.x);
     uint32_t it = 0;
     for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
-      const uint32_t ids = ids_next;
+      uint32_t ids = ids_next;
       ids_next = key_ids(id + G);
+      if (ids >= nblk) {
+        raise_flag(p.flag, llsa_dev::kErrIndex);
+        ids = 0;
+      }
       const uint32_t kb = it % Lay::kKeyBufs;
       if (it >= (uint32_t)Lay::kKeyBufs)
         mbar_wait(bar(KEMPTY + kb), ((it / Lay::kKeyBufs) - 1) & 1);
