@@ -146,6 +146,22 @@ __global__ void __launch_bounds__(256) select_level_kernel(
   }
 }
 
+// Packed fp32x2 arithmetic (sm_100): two exact IEEE products / sums per
+// instruction.  The product is an fma with a -0 addend read from memory, so
+// ptxas cannot contract it with the following add (it fuses a plain
+// mul.rn.f32x2 + add.rn.f32x2 pair into FFMA2); fma(a, b, -0) rounds the
+// exact product once, like mul.rn, including signed zeros.
+__device__ __forceinline__ uint64_t mul2_exact(uint64_t a, uint64_t b, uint64_t nz) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(nz));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // Fast variant for d % 4 == 0, B = 16 query rows per block, C = K·B <= 256
 // candidates, K <= 32: thread (row r, lane group cg) scores candidates
 // cg, cg+16, … with q_r and the candidate rows streamed as float4 from smem
@@ -157,7 +173,7 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
     const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
     uint64_t k_unit_stride, const uint32_t* __restrict__ parent, uint64_t parent_unit_stride,
     uint32_t parent_k, uint32_t key_blocks, uint32_t d, uint32_t K, float scale,
-    uint32_t* __restrict__ out, uint64_t out_unit_stride, uint32_t* flag) {
+    uint32_t* __restrict__ out, uint64_t out_unit_stride, uint32_t* flag, uint64_t negzero2) {
   constexpr uint32_t B = 16;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t blk = blockIdx.x, unit = blockIdx.y;
@@ -183,39 +199,48 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
     reinterpret_cast<float4*>(sq + r * ld)[j] = reinterpret_cast<const float4*>(qu + r * d)[j];
   }
   __syncthreads();
+  // candidate rows: global → smem with cp.async (no register round trip, so
+  // a thread's copies are all in flight at once)
   const float* ku = k + unit * k_unit_stride;
+  const uint32_t sk_s = (uint32_t)__cvta_generic_to_shared(sk);
   for (uint32_t e = threadIdx.x; e < C * d4; e += blockDim.x) {
     const uint32_t c = e / d4, j = e % d4;
-    reinterpret_cast<float4*>(sk + c * ld)[j] =
-        __ldg(reinterpret_cast<const float4*>(ku + (uint64_t)ids[c] * d) + j);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sk_s + (c * ld + 4 * j) * 4),
+                 "l"(ku + (uint64_t)ids[c] * d + 4 * j)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   {
     const uint32_t r = threadIdx.x >> 4, cg = threadIdx.x & 15;
-    float acc[CPT][4];
+    // accumulators (s0, s1) and (s2, s3) of each pair as packed fp32x2: the
+    // same per-lane operations and order as detail::dot
+    uint64_t acc[CPT][2];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    const float4* qr = reinterpret_cast<const float4*>(sq + r * ld);
+    for (int i = 0; i < CPT; ++i) acc[i][0] = acc[i][1] = 0ull;
+    const ulonglong2* qr = reinterpret_cast<const ulonglong2*>(sq + r * ld);
     for (uint32_t j = 0; j < d4; ++j) {
-      const float4 x = qr[j];
+      const ulonglong2 x = qr[j];
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
         const uint32_t c = cg + 16 * i;
         if (c < C) {
-          const float4 y = reinterpret_cast<const float4*>(sk + c * ld)[j];
-          acc[i][0] = __fadd_rn(acc[i][0], __fmul_rn(x.x, y.x));
-          acc[i][1] = __fadd_rn(acc[i][1], __fmul_rn(x.y, y.y));
-          acc[i][2] = __fadd_rn(acc[i][2], __fmul_rn(x.z, y.z));
-          acc[i][3] = __fadd_rn(acc[i][3], __fmul_rn(x.w, y.w));
+          const ulonglong2 y = reinterpret_cast<const ulonglong2*>(sk + c * ld)[j];
+          acc[i][0] = add2(acc[i][0], mul2_exact(x.x, y.x, negzero2));
+          acc[i][1] = add2(acc[i][1], mul2_exact(x.y, y.y, negzero2));
         }
       }
     }
 #pragma unroll
     for (int i = 0; i < CPT; ++i) {
       const uint32_t c = cg + 16 * i;
-      if (c < C)
-        scores[r * 256 + c] = __fmul_rn(
-            scale, __fadd_rn(__fadd_rn(acc[i][0], acc[i][1]), __fadd_rn(acc[i][2], acc[i][3])));
+      if (c < C) {
+        const float s0 = __uint_as_float((uint32_t)acc[i][0]);
+        const float s1 = __uint_as_float((uint32_t)(acc[i][0] >> 32));
+        const float s2 = __uint_as_float((uint32_t)acc[i][1]);
+        const float s3 = __uint_as_float((uint32_t)(acc[i][1] >> 32));
+        scores[r * 256 + c] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+      }
     }
   }
   __syncthreads();
@@ -310,7 +335,7 @@ llsa_status launch_select_level(const float* q, uint64_t q_unit_stride, const fl
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<dim3(parent_rows, units), 256, smem, s>>>(
           q, q_unit_stride, k, k_unit_stride, parent, parent_unit_stride, parent_k, key_blocks,
-          d, K, scale, out, out_unit_stride, device_flag());
+          d, K, scale, out, out_unit_stride, device_flag(), 0x8000000080000000ull);
       count_launch();
       LLSA_LAUNCH_CHECK("select_level_fast_kernel");
       return LLSA_OK;
