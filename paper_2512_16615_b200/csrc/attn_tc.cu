@@ -2066,9 +2066,10 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const int i0 = e2 * 16 + half * 8 + k * 2;
-                  const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
-                  const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
-                  pk[k] = pack_bf16(p0, p1);
+                  const float2 x = __ffma2_rn(
+                      make_float2(__uint_as_float(sv[i0]), __uint_as_float(sv[i0 + 1])),
+                      make_float2(c2, c2), make_float2(nb, nb));
+                  pk[k] = pack_bf16(ex2(x.x), ex2(x.y));
                 }
                 asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
                                  sp + swz(row, e * 2 + half)),
@@ -2494,10 +2495,15 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
 #pragma unroll
                   for (int k = 0; k < 4; ++k) {
                     const int i0 = ee * 16 + half * 8 + k * 2;
-                    const float p0 = ex2(fmaf(__uint_as_float(sv[i0]), c2, nb));
-                    const float p1 = ex2(fmaf(__uint_as_float(sv[i0 + 1]), c2, nb));
-                    pk[k] = pack_bf16(p0 * (__uint_as_float(gv[i0]) - Drow),
-                                      p1 * (__uint_as_float(gv[i0 + 1]) - Drow));
+                    // packed fp32x2: same per-element operations and rounding
+                    const float2 x = __ffma2_rn(
+                        make_float2(__uint_as_float(sv[i0]), __uint_as_float(sv[i0 + 1])),
+                        make_float2(c2, c2), make_float2(nb, nb));
+                    const float2 g = __fadd2_rn(
+                        make_float2(__uint_as_float(gv[i0]), __uint_as_float(gv[i0 + 1])),
+                        make_float2(-Drow, -Drow));
+                    const float2 ds = __fmul2_rn(make_float2(ex2(x.x), ex2(x.y)), g);
+                    pk[k] = pack_bf16(ds.x, ds.y);
                   }
                   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
                                    sds + swz(row, e * 2 + half)),
