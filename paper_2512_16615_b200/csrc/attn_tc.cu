@@ -450,10 +450,20 @@ __device__ __forceinline__ void attend_dq(uint32_t kHi, uint32_t kLo, uint32_t v
         g[h][i] += gl[h][i];
       }
     }
-    x[0] = ex2(fmaf(x[0], c, bias) - lse0) * (y[0] - D0);
-    x[1] = ex2(fmaf(x[1], c, bias) - lse0) * (y[1] - D0);
-    x[2] = ex2(fmaf(x[2], c, bias) - lse1) * (y[2] - D1);
-    x[3] = ex2(fmaf(x[3], c, bias) - lse1) * (y[3] - D1);
+    // packed fp32x2 (rows r: elements 0, 1; row r+8: 2, 3), same rounding
+    const float2 c22 = make_float2(c, c), b22 = make_float2(bias, bias);
+    const float2 t01 = __fadd2_rn(__ffma2_rn(make_float2(x[0], x[1]), c22, b22),
+                                  make_float2(-lse0, -lse0));
+    const float2 t23 = __fadd2_rn(__ffma2_rn(make_float2(x[2], x[3]), c22, b22),
+                                  make_float2(-lse1, -lse1));
+    const float2 g01 = __fadd2_rn(make_float2(y[0], y[1]), make_float2(-D0, -D0));
+    const float2 g23 = __fadd2_rn(make_float2(y[2], y[3]), make_float2(-D1, -D1));
+    const float2 r01 = __fmul2_rn(make_float2(ex2(t01.x), ex2(t01.y)), g01);
+    const float2 r23 = __fmul2_rn(make_float2(ex2(t23.x), ex2(t23.y)), g23);
+    x[0] = r01.x;
+    x[1] = r01.y;
+    x[2] = r23.x;
+    x[3] = r23.y;
   }
   const uint32_t a[4] = {pack_bf16(s[0][0], s[0][1]), pack_bf16(s[0][2], s[0][3]),
                          pack_bf16(s[1][0], s[1][1]), pack_bf16(s[1][2], s[1][3])};
@@ -2975,13 +2985,18 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         uint32_t ds[8], pp[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          float p0 = ex2(fmaf(__uint_as_float(sv[2 * k]), c2, nb));
-          float p1 = ex2(fmaf(__uint_as_float(sv[2 * k + 1]), c2, nb));
-          float d0 = p0 * (__uint_as_float(sv[16 + 2 * k]) - Dr);
-          float d1 = p1 * (__uint_as_float(sv[16 + 2 * k + 1]) - Dr);
-          if (!valid) p0 = p1 = d0 = d1 = 0.f;
-          pp[k] = pack_bf16(p0, p1);
-          ds[k] = pack_bf16(d0, d1);
+          // packed fp32x2: same per-element operations and rounding
+          const float2 x = __ffma2_rn(
+              make_float2(__uint_as_float(sv[2 * k]), __uint_as_float(sv[2 * k + 1])),
+              make_float2(c2, c2), make_float2(nb, nb));
+          float2 pe = make_float2(ex2(x.x), ex2(x.y));
+          const float2 g = __fadd2_rn(
+              make_float2(__uint_as_float(sv[16 + 2 * k]), __uint_as_float(sv[17 + 2 * k])),
+              make_float2(-Dr, -Dr));
+          float2 de = __fmul2_rn(pe, g);
+          if (!valid) pe = de = make_float2(0.f, 0.f);
+          pp[k] = pack_bf16(pe.x, pe.y);
+          ds[k] = pack_bf16(de.x, de.y);
         }
         if (c >= 2) mbar_wait(bar(BFREE + b), ((c >> 1) - 1) & 1);
         const uint32_t sb = sbase + kOffB + b * 16384;
@@ -3333,16 +3348,21 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         uint32_t pk[4], dk4[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          float pe[2], de[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = c8 * 8 + h * 2 + e;
-            const float pr = ex2(fmaf(__uint_as_float(sv[i]), c2, bias - lse[i]));
-            pe[e] = pr;
-            de[e] = pr * (__uint_as_float(pv[i]) - Dq[i]);
-          }
-          pk[h] = pack_bf16(pe[0], pe[1]);
-          dk4[h] = pack_bf16(de[0], de[1]);
+          // packed fp32x2 over queries i, i+1: same per-element rounding
+          const int i = c8 * 8 + h * 2;
+          const float2 l2 = *reinterpret_cast<const float2*>(lse + i);
+          const float2 d2 = *reinterpret_cast<const float2*>(Dq + i);
+          const float2 nb2 = __fadd2_rn(make_float2(bias, bias), make_float2(-l2.x, -l2.y));
+          const float2 x = __ffma2_rn(
+              make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])),
+              make_float2(c2, c2), nb2);
+          const float2 pe = make_float2(ex2(x.x), ex2(x.y));
+          const float2 g = __fadd2_rn(
+              make_float2(__uint_as_float(pv[i]), __uint_as_float(pv[i + 1])),
+              make_float2(-d2.x, -d2.y));
+          const float2 de = __fmul2_rn(pe, g);
+          pk[h] = pack_bf16(pe.x, pe.y);
+          dk4[h] = pack_bf16(de.x, de.y);
         }
         const uint32_t chunk = qh * 4 + c8;
         asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(sPT + swz(krow, chunk)),
