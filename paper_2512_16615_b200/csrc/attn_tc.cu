@@ -275,7 +275,7 @@ constexpr int kFStage = 2 * kTile16;           // 4 KB
 constexpr int kFwdSmem = 2 * kFwdCStage + 8 * 2 * kFStage + 2 * kMaxCoarse * 4;  // 112.5 KB
 
 __global__ void __launch_bounds__(256, 2) tc_fwd_kernel(TcParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t unit = blockIdx.y;
   const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
@@ -483,7 +483,7 @@ constexpr int kDqCStage = 4 * kDqArr;         // 16 KB
 constexpr int kDqSmem = 2 * kDqCStage + 8 * 2 * kFStage + 2 * kMaxCoarse * 4;  // 96.5 KB
 
 __global__ void __launch_bounds__(256, 2) tc_dq_kernel(TcParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t unit = blockIdx.y;
   const uint64_t q0 = (uint64_t)blockIdx.x * kTileQ;
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
   constexpr bool use_lo = MODE == 2;
   using Cfg = KvCfg<COARSE>;
   constexpr int QC = Cfg::QC, NT = QC / 8;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t gw = (uint64_t)blockIdx.x * kKvWarps + warp;
   const uint32_t unit = (uint32_t)(gw / tasks_per_unit);
@@ -2171,7 +2171,6 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
     uint32_t i = 0;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
       const uint32_t unit = (uint32_t)(id / tpu);
-      const uint64_t q0 = (id % tpu) * kTileQ;
       const uint32_t qs = i % kQStages;
       const uint64_t in_off = (uint64_t)unit * p.n * kD;
       const uint32_t myb = next_ids;
@@ -2292,12 +2291,6 @@ constexpr uint32_t kTmemCols = 512;  // S/dP x 2 [0, 256), dQ_c x 2 [256, 384), 
 constexpr uint32_t kMaxEntries = 24;  // ent_rows[24]
 }  // namespace dqf
 
-// fp32 [128][64] staging with 8-float groups XOR-swizzled by row (conflict-free
-// row-wise float4 reads, 2-way fragment writes)
-__device__ __forceinline__ uint32_t dqf_idx(uint32_t row, uint32_t col) {
-  return row * 64u + (col ^ ((row & 7u) << 3));
-}
-
 __global__ void __launch_bounds__(dqf::kThreads, 1)
     tc5_dqf_kernel(const __grid_constant__ TcParams p, const __grid_constant__ TmaMaps m,
                    uint32_t units) {
@@ -2311,7 +2304,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   float* stat = reinterpret_cast<float*>(smem + kOffStat);  // [2 tiles][lse | D][128]
   float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
   uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
-  uint32_t* ent_rows = reinterpret_cast<uint32_t*>(smem + kOffEnt + 160);  // [24]
   const uint64_t tpu = p.n / kTileQ;
   const uint64_t total = tpu * units;
   const uint32_t nce = p.nce, nch = (nce + 3) / 4;
@@ -2564,7 +2556,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
     const uint32_t fw = 2 * (warp & 3) + (warp >= 11 ? 1u : 0u);
     const uint32_t sF = sbase + kOffFine + fw * kFineWarp;
     const uint64_t nfb = p.n / kBS;
-    const uint32_t r = lane >> 2, cc = (lane & 3) * 2;
+    const uint32_t r = lane >> 2;
     const Block16Lane bl = block16_lane(lane);
     auto fine_ids = [&](uint64_t id) -> uint32_t {
       if (id >= total || lane >= p.K) return 0u;
@@ -2770,15 +2762,6 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
-  // CSC segment of item `id`: (first flat index, length)
-  auto segment = [&](uint64_t id, uint32_t& unit, uint64_t& kb, const uint32_t*& seg) {
-    unit = (uint32_t)(id / nkb);
-    kb = id % nkb;
-    const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[0];
-    seg = p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[0] + off[kb];
-    return off[kb + 1] - off[kb];
-  };
-
   if (warp == 0 || warp == 2 || warp == 11 || warp == 12) {
     // ------------------------------------------------------------ gather
     // Four warps share every chunk (warp gi: query blocks gi and gi + 4;
@@ -2789,7 +2772,6 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     // proxy after the wait.
     const uint32_t gi = warp == 0 ? 0u : warp == 2 ? 1u : warp - 9;
     const Block16Lane bl = block16_lane(lane);
-    const uint64_t nqb = p.n / kBS;
     // Item facts (CSC segment bounds, first 32 query-block ids) come from the
     // facts warp through a smem ring filled up to 8 items ahead, so no
     // dependent global load sits on the issue path.

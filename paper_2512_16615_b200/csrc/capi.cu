@@ -408,7 +408,7 @@ llsa_status llsa_transpose_indices(const uint32_t* idx, uint32_t units, uint32_t
                                    uint32_t* flat, void* ws, size_t ws_bytes, void* stream) {
   if (units == 0) return LLSA_OK;
   NONNULL(offsets);
-  if ((uint64_t)rows * k) {
+  if (rows != 0 && k != 0) {
     NONNULL(idx);
     NONNULL(flat);
   }
