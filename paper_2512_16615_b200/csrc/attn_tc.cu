@@ -2486,6 +2486,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             tmem_ld32(tmem + lane_off + b * 128 + 32 * hh, sv);
             tmem_ld32(tmem + lane_off + b * 128 + 64 + 32 * hh, gv);
             tmem_ld_wait();
+            if (2 * hh + 2 >= (int)ne) {  // S / dP all in registers: release the buffer
+              fence_before();
+              mbar_arrive(bar(TFREE + b));
+            }
 #pragma unroll
             for (int ee = 0; ee < 2; ++ee) {
               const uint32_t e = 2 * hh + ee;
@@ -2515,8 +2519,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             }
           }
         }
-        fence_before();
-        mbar_arrive(bar(TFREE + b));
         fence_proxy_async();
         mbar_arrive(bar(DSREADY + b));
         if (tid == 96) trace_ev(p, 4, c, 0);
