@@ -1151,29 +1151,43 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level];
   const float* part = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li];
   const uint32_t tok = threadIdx.x >> 4, c4 = (threadIdx.x & 15) * 4;
+  // the segment's (row, position of b in the row) pairs are resolved by one
+  // thread each into smem first, so the summation below issues independent
+  // loads instead of a seg → table → partial chain per row
+  __shared__ uint32_t s_row[256], s_pos[256];
   float4 ak = make_float4(0.f, 0.f, 0.f, 0.f), av = ak;
-  for (uint32_t si = 0; si < len; ++si) {
-    const uint32_t r = seg[si];
-    uint32_t pos = 0;
-    for (uint32_t j = 0; j < p.K; ++j)
-      if (tab[(uint64_t)r * p.K + j] == b) pos = j;
-    const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
-    const float* src0 = part + ((uint64_t)r * slices * p.groups + g) * (2 * rows::kKeys * kD) +
-                        (uint64_t)key * kD + c4;
-#pragma unroll 4
-    for (uint32_t s = 0; s < slices; ++s) {
-      const float* src = src0 + (uint64_t)s * p.groups * (2 * rows::kKeys * kD);
-      const float4 x = __ldg(reinterpret_cast<const float4*>(src));
-      const float4 y = __ldg(reinterpret_cast<const float4*>(src + rows::kKeys * kD));
-      ak.x += x.x;
-      ak.y += x.y;
-      ak.z += x.z;
-      ak.w += x.w;
-      av.x += y.x;
-      av.y += y.y;
-      av.z += y.z;
-      av.w += y.w;
+  for (uint32_t base = 0; base < len; base += 256) {
+    const uint32_t nrow = min(256u, len - base);
+    if (threadIdx.x < nrow) {
+      const uint32_t r = seg[base + threadIdx.x];
+      uint32_t pos = 0;
+      for (uint32_t j = 0; j < p.K; ++j)
+        if (tab[(uint64_t)r * p.K + j] == b) pos = j;
+      s_row[threadIdx.x] = r;
+      s_pos[threadIdx.x] = pos;
     }
+    __syncthreads();
+    for (uint32_t si = 0; si < nrow; ++si) {
+      const uint32_t r = s_row[si], pos = s_pos[si];
+      const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
+      const float* src0 = part + ((uint64_t)r * slices * p.groups + g) * (2 * rows::kKeys * kD) +
+                          (uint64_t)key * kD + c4;
+#pragma unroll 4
+      for (uint32_t s = 0; s < slices; ++s) {
+        const float* src = src0 + (uint64_t)s * p.groups * (2 * rows::kKeys * kD);
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+        const float4 y = __ldg(reinterpret_cast<const float4*>(src + rows::kKeys * kD));
+        ak.x += x.x;
+        ak.y += x.y;
+        ak.z += x.z;
+        ak.w += x.w;
+        av.x += y.x;
+        av.y += y.y;
+        av.z += y.z;
+        av.w += y.w;
+      }
+    }
+    __syncthreads();
   }
   // slot of this level in the coarse-slot table (levels 1..lim-1 come first)
   uint32_t sl = 0;
