@@ -246,16 +246,18 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
   __syncthreads();
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (uint32_t r = warp; r < B; r += blockDim.x >> 5) {
-    // lane owns positions lane*8 .. lane*8+7 (contiguous, so position order =
-    // (lane, i) order).  Scores become order-preserving u32 keys (-0 → +0, the
-    // float compare ties them); each round takes the warp max key with
-    // redux.sync and, among equal keys, the lowest position (topk_row's
-    // lowest-index tie-break), so the selection is exact.
-    uint32_t key[8];
+    // lane owns positions lane*PL .. lane*PL+PL-1 (contiguous, so position
+    // order = (lane, i) order; PL = 4 covers C <= 128 with every lane busy).
+    // Scores become order-preserving u32 keys (-0 → +0, the float compare
+    // ties them); each round takes the warp max key with redux.sync and,
+    // among equal keys, the lowest position (topk_row's lowest-index
+    // tie-break), so the selection is exact.
+    constexpr int PL = CPT / 2;
+    uint32_t key[PL];
     uint32_t taken = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t c = lane * 8 + i;
+    for (int i = 0; i < PL; ++i) {
+      const uint32_t c = lane * PL + i;
       float v = c < C ? scores[r * 256 + c] : 0.f;
       if (v == 0.f) v = 0.f;  // canonical +0
       const uint32_t u = __float_as_uint(v);
@@ -264,18 +266,18 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
     for (uint32_t round = 0; round < K; ++round) {
       uint32_t lk = key[0], li = 0;
 #pragma unroll
-      for (int i = 1; i < 8; ++i)
+      for (int i = 1; i < PL; ++i)
         if (key[i] > lk) {
           lk = key[i];
           li = i;
         }
       const uint32_t mk = __reduce_max_sync(0xffffffffu, lk);
-      const uint32_t mypos = lk == mk && lk != 0u ? lane * 8 + li : 0xffffffffu;
+      const uint32_t mypos = lk == mk && lk != 0u ? lane * PL + li : 0xffffffffu;
       const uint32_t bpos = __reduce_min_sync(0xffffffffu, mypos);
       if (bpos == mypos) {
         taken |= 1u << li;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < PL; ++i)
           if ((uint32_t)i == li) key[i] = 0u;
       }
     }
@@ -289,8 +291,8 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
     uint32_t pos = pre - cnt;
     uint32_t* o = out + unit * out_unit_stride + ((uint64_t)blk * B + r) * K;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if ((taken >> i) & 1u) o[pos++] = ids[lane * 8 + i];
+    for (int i = 0; i < PL; ++i)
+      if ((taken >> i) & 1u) o[pos++] = ids[lane * PL + i];
   }
 }
 
