@@ -194,8 +194,16 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
   }
   const float* qu = q + unit * q_unit_stride + (uint64_t)blk * B * d;
   const uint32_t d4 = d / 4;
+  // row / column of flat float4 index e (shift and mask when d/4 is a power of 2)
+  const bool pow2 = (d4 & (d4 - 1)) == 0;
+  const uint32_t sh = __ffs(d4) - 1;
+  auto rc = [&](uint32_t e, uint32_t& r, uint32_t& j) {
+    r = pow2 ? e >> sh : e / d4;
+    j = pow2 ? e & (d4 - 1) : e % d4;
+  };
   for (uint32_t e = threadIdx.x; e < B * d4; e += blockDim.x) {
-    const uint32_t r = e / d4, j = e % d4;
+    uint32_t r, j;
+    rc(e, r, j);
     reinterpret_cast<float4*>(sq + r * ld)[j] = reinterpret_cast<const float4*>(qu + r * d)[j];
   }
   __syncthreads();
@@ -204,7 +212,8 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
   const float* ku = k + unit * k_unit_stride;
   const uint32_t sk_s = (uint32_t)__cvta_generic_to_shared(sk);
   for (uint32_t e = threadIdx.x; e < C * d4; e += blockDim.x) {
-    const uint32_t c = e / d4, j = e % d4;
+    uint32_t c, j;
+    rc(e, c, j);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sk_s + (c * ld + 4 * j) * 4),
                  "l"(ku + (uint64_t)ids[c] * d + 4 * j)
                  : "memory");
