@@ -2727,13 +2727,14 @@ constexpr int kOffInfo = kOffB + 2 * 16384;    // per-stage chunk facts
 constexpr int kFactSlots = 8, kFactWords = 36;  // item facts ring: lo, hi, ids[32]
 constexpr int kOffFacts = kOffInfo + 64;
 constexpr int kOffBar = kOffFacts + kFactSlots * kFactWords * 4;
+constexpr int kAB = 4;  // Acc buffers (items in flight between MMA and epilogue)
 enum { FULL = 0, EMPTY = kRing, SREADY = 2 * kRing, SFREE = SREADY + 2, BREADY = SFREE + 2,
-       BFREE = BREADY + 2, AREADY = BFREE + 2, AFREE = AREADY + 2, FACTF = AFREE + 2,
+       BFREE = BREADY + 2, AREADY = BFREE + 2, AFREE = AREADY + kAB, FACTF = AFREE + kAB,
        FACTE = FACTF + kFactSlots, NBAR = FACTE + kFactSlots };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
 // gather 0, 2, 11, 12; MMA 1, 13; softmax 3-6; epilogue 7-10; item facts 14
 constexpr int kThreads = 15 * 32;
-constexpr uint32_t kTmemCols = 256;  // S|dP x 2 at [0, 64), Acc x 2 at 64, 128
+constexpr uint32_t kTmemCols = 512;  // S|dP x 2 at [0, 64), Acc x kAB at 64 + 64·i
 }  // namespace kvf
 
 __global__ void __launch_bounds__(kvf::kThreads, 1)
@@ -2765,6 +2766,8 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       mbar_init(bar(SFREE + i), 128);
       mbar_init(bar(BREADY + i), 128);
       mbar_init(bar(BFREE + i), 1);
+    }
+    for (int i = 0; i < kAB; ++i) {
       mbar_init(bar(AREADY + i), 1);
       mbar_init(bar(AFREE + i), 128);
     }
@@ -2933,11 +2936,11 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         const uint32_t inf = info[s];
         if (inf & 0x400u) break;
         const uint32_t mc = inf & 0xFF, first = (inf >> 8) & 1, last = (inf >> 9) & 1;
-        const uint32_t ab = ai & 1;
+        const uint32_t ab = ai % kAB;
         trace_ev(p, 6, c, 0);
         mbar_wait(bar(BREADY + b), (c >> 1) & 1);
         trace_ev(p, 6, c, 1);
-        if (first && ai >= 2) mbar_wait(bar(AFREE + ab), ((ai >> 1) - 1) & 1);
+        if (first && ai >= (uint32_t)kAB) mbar_wait(bar(AFREE + ab), ((ai / kAB) - 1) & 1);
         fence_proxy_async();
         fence_after();
         const uint32_t st = sbase + s * kStage;
@@ -3056,9 +3059,9 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       const uint64_t kb = id % nkb;
       float acc[16];
       if (m) {
-        const uint32_t ab = ai & 1;
+        const uint32_t ab = ai % kAB;
         if (tid == 224) trace_ev(p, 5, ai, 0);
-        mbar_wait(bar(AREADY + ab), (ai >> 1) & 1);
+        mbar_wait(bar(AREADY + ab), (ai / kAB) & 1);
         if (tid == 224) trace_ev(p, 5, ai, 1);
         fence_after();
         uint32_t r[16];
