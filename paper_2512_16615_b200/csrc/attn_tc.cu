@@ -76,7 +76,8 @@ struct TcParams {
   // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
   // shallower ones (gain B^l small) use hi only.
   uint32_t hilo_level;
-  uint32_t dbg;    // debug toggles (LLSA_DBG)
+  uint32_t dbg;    // debug probes (LLSA_DBG): 8 skip fine attention, 16 skip fine gathers
+                   // (forward, dQ) — timing only, results are wrong
   uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
@@ -2195,8 +2196,10 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           b = 0;
         }
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
-        load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        if (!(p.dbg & 16)) {  // probe: LLSA_DBG bit 16 skips the fine gathers
+          load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
+          load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
+        }
       };
 #pragma unroll
       for (uint32_t j = 0; j + 1 < (uint32_t)kFineStages; ++j) {
@@ -2227,7 +2230,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         cp_async_wait<kFineStages - 1>();
         __syncwarp();
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        attend_fine(base, base + kTile16, bf, c2, qf, lane, st);
+        if (!(p.dbg & 8)) attend_fine(base, base + kTile16, bf, c2, qf, lane, st);  // probe
         __syncwarp();
       }
       // publish the fine partition (raw O_f, m_f, l_f) for the coarse warps
