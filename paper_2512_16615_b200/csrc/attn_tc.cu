@@ -76,8 +76,7 @@ struct TcParams {
   // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
   // shallower ones (gain B^l small) use hi only.
   uint32_t hilo_level;
-  uint32_t dbg;    // debug probes (LLSA_DBG): 8 skip fine attention, 16 skip fine gathers
-                   // (forward, dQ) — timing only, results are wrong
+  uint32_t dbg;    // LLSA_DBG: timing probes, see probe()
   uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
@@ -103,6 +102,20 @@ struct TcParams {
 // Pipeline trace (debug only): CTA 0 records (role, tile, event, clock) so the
 // hand-offs of the warp-specialised kernels can be inspected offline.
 __device__ unsigned long long g_trace[8192];  // [role 0..7][tile 0..31][event 0..31]
+// Timing probes, compiled in only with -DLLSA_PROBES (LLSA_NVCC_EXTRA): with
+// them LLSA_DBG bit 8 skips the fine attention and bit 16 the fine gathers of
+// the forward and dQ kernels (results are then wrong).  A runtime check in
+// the fine loops costs ~10 us of forward time, hence the macro.
+__device__ __forceinline__ bool probe(const TcParams& p, uint32_t bit) {
+#ifdef LLSA_PROBES
+  return p.dbg & bit;
+#else
+  (void)p;
+  (void)bit;
+  return false;
+#endif
+}
+
 __device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t role, uint32_t tile,
                                          uint32_t ev) {
   if (p.trace && blockIdx.x == 0 && tile < 32 && ev < 32)
@@ -2196,7 +2209,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           b = 0;
         }
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        if (!(p.dbg & 16)) {  // probe: LLSA_DBG bit 16 skips the fine gathers
+        if (!probe(p, 16)) {
           load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
           load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
         }
@@ -2230,7 +2243,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         cp_async_wait<kFineStages - 1>();
         __syncwarp();
         const uint32_t base = sF + (j % kFineStages) * 4096;
-        if (!(p.dbg & 8)) attend_fine(base, base + kTile16, bf, c2, qf, lane, st);  // probe
+        if (!probe(p, 8)) attend_fine(base, base + kTile16, bf, c2, qf, lane, st);
         __syncwarp();
       }
       // publish the fine partition (raw O_f, m_f, l_f) for the coarse warps
@@ -2598,7 +2611,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           b = 0;
         }
         const uint32_t base = sF + (j % kFS) * 4096;
-        if (!(p.dbg & 16)) {
+        if (!probe(p, 16)) {
           load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
           load_block16_async(base + kTile16, p.v + in_off + (uint64_t)b * kBS * kD, bl, lane);
         }
@@ -2674,7 +2687,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         cp_async_wait<kFS - 1>();
         __syncwarp();
         const uint32_t base = sF + (j % kFS) * 4096;
-        if (!(p.dbg & 8)) attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
+        if (!probe(p, 8)) attend_dq<false>(base, base, base + kTile16, base + kTile16, 0, bf, c2, qf, gf, lse0,
                          lse1, D0, D1, lane, dq);
         __syncwarp();
       }
