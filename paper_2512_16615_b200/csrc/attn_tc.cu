@@ -116,10 +116,19 @@ __device__ __forceinline__ bool probe(const TcParams& p, uint32_t bit) {
 #endif
 }
 
+// Pipeline timestamps of CTA 0 (tools/trace_fwd.py), compiled in only with
+// -DLLSA_TRACE_EVENTS so the hot loops carry no runtime check.
 __device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t role, uint32_t tile,
                                          uint32_t ev) {
+#ifdef LLSA_TRACE_EVENTS
   if (p.trace && blockIdx.x == 0 && tile < 32 && ev < 32)
     g_trace[role * 1024 + tile * 32 + ev] = clock64() | (1ull << 63);
+#else
+  (void)p;
+  (void)role;
+  (void)tile;
+  (void)ev;
+#endif
 }
 
 // Coarse entry e of the tile whose first fine block is fb0 → (level, first

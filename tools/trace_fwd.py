@@ -1,5 +1,7 @@
 """Debug: runs one forward with LLSA_TRACE=1 and prints CTA 0's pipeline
-timeline (role, tile, event, cycle offset)."""
+timeline (role, tile, event, cycle offset).  Needs a build with the events
+compiled in:  LLSA_NVCC_EXTRA=-DLLSA_TRACE_EVENTS python -m
+paper_2512_16615_b200._build --force"""
 import ctypes as C
 import os
 import sys
