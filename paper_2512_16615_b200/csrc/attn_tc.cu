@@ -2210,13 +2210,13 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint32_t qs = i % kQStages;
       const uint64_t in_off = (uint64_t)unit * p.n * kD;
-      const uint32_t myb = next_ids;
+      uint32_t myb = next_ids;  // the tile's block ids, range-checked once per tile
+      if (myb >= nfb) {
+        raise_flag(p.flag, llsa_dev::kErrIndex);
+        myb = 0;
+      }
       auto load_fine = [&](uint32_t j) {
-        uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
-        if (b >= nfb) {
-          raise_flag(p.flag, llsa_dev::kErrIndex);
-          b = 0;
-        }
+        const uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
         const uint32_t base = sF + (j % kFineStages) * 4096;
         if (!probe(p, 16)) {
           load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
@@ -2612,13 +2612,13 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint64_t q0 = (id % tpu) * kTileQ;
       const uint64_t in_off = (uint64_t)unit * p.n * kD;
-      const uint32_t myb = next_ids;
+      uint32_t myb = next_ids;  // the tile's block ids, range-checked once per tile
+      if (myb >= nfb) {
+        raise_flag(p.flag, llsa_dev::kErrIndex);
+        myb = 0;
+      }
       auto load_fine = [&](uint32_t j) {
-        uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
-        if (b >= nfb) {
-          raise_flag(p.flag, llsa_dev::kErrIndex);
-          b = 0;
-        }
+        const uint32_t b = __shfl_sync(0xffffffffu, myb, j & 31);
         const uint32_t base = sF + (j % kFS) * 4096;
         if (!probe(p, 16)) {
           load_block16_async(base, p.k + in_off + (uint64_t)b * kBS * kD, bl, lane);
