@@ -2827,11 +2827,11 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       const uint32_t fs = it % kFactSlots;
       mbar_wait(bar(FACTF + fs), (it / kFactSlots) & 1);
       const uint32_t lo0 = fact[fs * kFactWords], hi0 = fact[fs * kFactWords + 1];
+      const uint32_t unit = fact[fs * kFactWords + 2];
+      const uint64_t kb = fact[fs * kFactWords + 3];
       const uint32_t ids0 = fact[fs * kFactWords + 4 + lane];
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(FACTE + fs));
-      const uint32_t unit = (uint32_t)(id / nkb);
-      const uint64_t kb = id % nkb;
       const uint32_t m = hi0 - lo0;
       const uint32_t* seg = flat0 + (uint64_t)unit * p.csc_flat_entries + lo0;
       const uint64_t in_off = (uint64_t)unit * p.n * kD, ro = (uint64_t)unit * p.n;
@@ -2915,8 +2915,11 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         const uint32_t l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
         if (it >= (uint32_t)kFactSlots) mbar_wait(bar(FACTE + j), ((it / kFactSlots) - 1) & 1);
         if (lane == 0) {
+          const uint64_t id = id0 + (uint64_t)j * G;
           fact[j * kFactWords] = l;
           fact[j * kFactWords + 1] = h;
+          fact[j * kFactWords + 2] = (uint32_t)(id / nkb);  // unit
+          fact[j * kFactWords + 3] = (uint32_t)(id % nkb);  // key block
         }
         fact[j * kFactWords + 4 + lane] = qb[j];
         __syncwarp();
