@@ -3422,6 +3422,10 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem + lane_off + 256 + 128 * ab + 32 * q4, r);
         tmem_ld_wait();
+        if (q4 == 3) {  // the accumulators are in registers: release them before storing
+          fence_before();
+          mbar_arrive(bar(AFREE + ab));
+        }
         float* d = dst + (q4 >= 2 ? kKeys * kD : 0) + 32 * (q4 & 1);
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
@@ -3429,8 +3433,6 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
               make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
                           __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
       }
-      fence_before();
-      mbar_arrive(bar(AFREE + ab));
     }
   }
   fence_before();
