@@ -2576,6 +2576,11 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         tmem_ld32(tmem + lane_off + 256 + tb * 64 + 32 * hh, r0);   // dQ_c
         tmem_ld32(tmem + lane_off + 384 + tb * 64 + 32 * hh, f);    // dQ_f (fine warps)
         tmem_ld_wait();
+        if (hh == 1) {  // both accumulators are in registers: release them first
+          fence_before();
+          mbar_arrive(bar(DQFREE + tb));
+          mbar_arrive(bar(FFREE + tb));
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           float4 v;
@@ -2586,9 +2591,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           reinterpret_cast<float4*>(d + 32 * hh)[k] = v;
         }
       }
-      fence_before();
-      mbar_arrive(bar(DQFREE + tb));
-      mbar_arrive(bar(FFREE + tb));
     }
   } else if (warp >= 7) {
     // ------------------------------------------------------------ fine warps
