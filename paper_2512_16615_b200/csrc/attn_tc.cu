@@ -3051,9 +3051,10 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     const uint32_t dcol = lane + 32 * (qd & 1);    // head-dim column
     const uint32_t lane_off = (32u * qd) << 16;
     // per item: segment length and the coarse pooled-adjoint rows for this
-    // column (B = 16 here: level-l row of token t is t >> 4l), loaded three
-    // items ahead into one of four register sets (the loop is unrolled by
-    // four so no loaded value is touched before its item)
+    // column (B = 16 here: level-l row of token t is t >> 4l), loaded one
+    // item ahead into one of two register sets (the loop is unrolled by two
+    // so no loaded value is moved or touched before its item; deeper
+    // unrolling grew the kernel past what the instruction cache holds)
     constexpr int kEL = 4;  // coarse level slots on this path (L <= 4)
     struct EpiFacts {
       uint32_t o0, o1;
@@ -3111,22 +3112,14 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
     };
     const uint64_t G = gridDim.x;
-    EpiFacts fa, fb, fc, fd;
+    EpiFacts fa, fb;
     issue(blockIdx.x, fa);
-    issue(blockIdx.x + G, fb);
-    issue(blockIdx.x + 2 * G, fc);
-    for (uint64_t id = blockIdx.x; id < total; id += 4 * G) {
-      issue(id + 3 * G, fd);
+    for (uint64_t id = blockIdx.x; id < total; id += 2 * G) {
+      issue(id + G, fb);
       body(id, fa);
       if (id + G >= total) break;
-      issue(id + 4 * G, fa);
+      issue(id + 2 * G, fa);
       body(id + G, fb);
-      if (id + 2 * G >= total) break;
-      issue(id + 5 * G, fb);
-      body(id + 2 * G, fc);
-      if (id + 3 * G >= total) break;
-      issue(id + 6 * G, fc);
-      body(id + 3 * G, fd);
     }
   }
   fence_before();
