@@ -2883,7 +2883,9 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
   } else if (warp == 14) {
     // ------------------------------------------------------------ item facts
     // batches of kFactSlots items: lane j loads the segment bounds of item
-    // k + j, then every item's first 32 query-block ids load in parallel
+    // k + j, then item by item the first 32 query-block ids (a loop, not
+    // unrolled: this warp runs up to 8 items ahead and its code shares the
+    // instruction cache with the hot roles)
     const uint32_t* off0 = p.csc_off + p.csc_off_off[0];
     const uint32_t* flat0 = p.csc_flat + p.csc_flat_off[0];
     uint32_t* fact = reinterpret_cast<uint32_t*>(smem + kOffFacts);
@@ -2901,29 +2903,22 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
           hi = o[1];
         }
       }
-      uint32_t qb[kFactSlots];
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < kFactSlots; ++j) {
         const uint64_t id = id0 + (uint64_t)j * G;
-        const uint32_t l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
-        qb[j] = id < total && l + lane < h
-                    ? flat0[(uint64_t)(id / nkb) * p.csc_flat_entries + l + lane]
-                    : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < kFactSlots; ++j) {
+        if (id >= total) break;
         const uint32_t it = k0 + j;
-        if (id0 + (uint64_t)j * G >= total) break;
         const uint32_t l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
+        const uint32_t qb =
+            l + lane < h ? flat0[(uint64_t)(id / nkb) * p.csc_flat_entries + l + lane] : 0u;
         if (it >= (uint32_t)kFactSlots) mbar_wait(bar(FACTE + j), ((it / kFactSlots) - 1) & 1);
         if (lane == 0) {
-          const uint64_t id = id0 + (uint64_t)j * G;
           fact[j * kFactWords] = l;
           fact[j * kFactWords + 1] = h;
           fact[j * kFactWords + 2] = (uint32_t)(id / nkb);  // unit
           fact[j * kFactWords + 3] = (uint32_t)(id % nkb);  // key block
         }
-        fact[j * kFactWords + 4 + lane] = qb[j];
+        fact[j * kFactWords + 4 + lane] = qb;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(FACTF + j));
       }
