@@ -335,3 +335,27 @@ def test_full_size_tensor_core_path_matches_simt(cfg):
         e = rel_err(got[0].cpu().numpy(), want[0].cpu().numpy())
         assert e["max_rel"] <= 2e-2, (name, e)
 
+
+
+# The persistent tcgen05 kernels walk (unit, tile) work items; a multi-unit
+# handle must give every unit exactly what a one-unit handle gives it.
+@pytest.mark.parametrize("n,L", [(16384, 2), (65536, 3)])
+def test_multi_unit_handle_is_per_unit_exact(n, L):
+    units = 3
+    g = torch.Generator(device="cuda").manual_seed(21)
+    q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
+                   for _ in range(4))
+    lc = llsa.LLSAConfig(n, 64, 16, 8, L, L)
+    hm = llsa.LLSAHandle(lc, units, torch.bfloat16)
+    assert hm.uses_tensor_cores
+    out = hm.forward(q, k, v)
+    grads = hm.backward(dO, q, k, v, out)
+    h1 = llsa.LLSAHandle(lc, 1, torch.bfloat16)
+    for u in range(units):
+        sl = slice(u, u + 1)
+        o1 = h1.forward(q[sl], k[sl], v[sl])
+        g1 = h1.backward(dO[sl], q[sl], k[sl], v[sl], o1)
+        assert torch.equal(out[sl], o1), u
+        for a, b in zip(grads, g1):
+            assert torch.equal(a[sl], b), u
+    llsa.sync_status()
