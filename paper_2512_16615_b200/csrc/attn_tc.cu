@@ -1123,10 +1123,11 @@ __global__ void __launch_bounds__(256, rows::Layout<LO>::kMinBlocks)
   cp_async_wait<0>();
   ensure_kv(ntiles);
   fence_after();
-  // raw partial sums of this task: [128 keys][64] dK', then dV'
+  // raw partial sums of this task, transposed: [64 d][128 keys] dK', then
+  // dV' (a warp's 32 keys of one d column are one 128-byte store)
   const uint64_t pidx = (row * slices + slice) * p.groups + group;
   float* dst = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li] +
-               pidx * (2 * kKeys * kD) + (qhalf ? kKeys * kD : 0) + (uint64_t)krow * kD;
+               pidx * (2 * kKeys * kD) + (qhalf ? kKeys * kD : 0) + krow;
   const uint32_t tsrc = (qhalf ? tDV : tDK) + lane_off;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
@@ -1134,10 +1135,7 @@ __global__ void __launch_bounds__(256, rows::Layout<LO>::kMinBlocks)
     tmem_ld32(tsrc + half * 32, r);
     tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4*>(dst + half * 32 + i) =
-          make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                      __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+    for (int i = 0; i < 32; ++i) dst[(uint64_t)(half * 32 + i) * kKeys] = __uint_as_float(r[i]);
   }
   fence_before();
   __syncthreads();
@@ -1173,7 +1171,9 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   const uint32_t len = off[b + 1] - off[b];
   const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level];
   const float* part = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li];
-  const uint32_t tok = threadIdx.x >> 4, c4 = (threadIdx.x & 15) * 4;
+  // thread = (token, 4 d columns) with the token fastest: the partials are
+  // [d][key], so 16 neighbouring lanes read 64 contiguous bytes per column
+  const uint32_t tok = threadIdx.x & 15, c4 = (threadIdx.x >> 4) * 4;
   // the segment's (row, position of b in the row) pairs are resolved by one
   // thread each into smem first, so the summation below issues independent
   // loads instead of a seg → table → partial chain per row
@@ -1194,12 +1194,15 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
       const uint32_t r = s_row[si], pos = s_pos[si];
       const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
       const float* src0 = part + ((uint64_t)r * slices * p.groups + g) * (2 * rows::kKeys * kD) +
-                          (uint64_t)key * kD + c4;
+                          (uint64_t)c4 * rows::kKeys + key;
 #pragma unroll 4
       for (uint32_t s = 0; s < slices; ++s) {
         const float* src = src0 + (uint64_t)s * p.groups * (2 * rows::kKeys * kD);
-        const float4 x = __ldg(reinterpret_cast<const float4*>(src));
-        const float4 y = __ldg(reinterpret_cast<const float4*>(src + rows::kKeys * kD));
+        const float* srv = src + rows::kKeys * kD;
+        const float4 x = make_float4(__ldg(src), __ldg(src + rows::kKeys),
+                                     __ldg(src + 2 * rows::kKeys), __ldg(src + 3 * rows::kKeys));
+        const float4 y = make_float4(__ldg(srv), __ldg(srv + rows::kKeys),
+                                     __ldg(srv + 2 * rows::kKeys), __ldg(srv + 3 * rows::kKeys));
         ak.x += x.x;
         ak.y += x.y;
         ak.z += x.z;
@@ -3404,11 +3407,13 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       const uint32_t ab = it & 1;
       mbar_wait(bar(AREADY + ab), (it >> 1) & 1);
       fence_after();
+      // transposed partial [64 d][128 keys] (dK', then dV'): for one d a
+      // warp's 32 keys are one coalesced 128-byte store
       const uint64_t pidx = (row * slices + slice) * p.groups + group;
       float* dst = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li] +
-                   pidx * (2 * kKeys * kD) + (uint64_t)krow * kD;
+                   pidx * (2 * kKeys * kD) + krow;
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {  // dK' cols 0-63 then dV' (+64 in TMEM, +128 rows in HBM)
+      for (int q4 = 0; q4 < 4; ++q4) {  // dK' cols 0-63 then dV' (+64 in TMEM)
         uint32_t r[32];
         tmem_ld32(tmem + lane_off + 256 + 128 * ab + 32 * q4, r);
         tmem_ld_wait();
@@ -3416,12 +3421,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
           fence_before();
           mbar_arrive(bar(AFREE + ab));
         }
-        float* d = dst + (q4 >= 2 ? kKeys * kD : 0) + 32 * (q4 & 1);
+        float* d = dst + (q4 >= 2 ? kKeys * kD : 0) + (uint64_t)(32 * (q4 & 1)) * kKeys;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(d + i) =
-              make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+        for (int i = 0; i < 32; ++i) d[(uint64_t)i * kKeys] = __uint_as_float(r[i]);
       }
     }
   }
