@@ -2572,7 +2572,12 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       mbar_wait(bar(FDONE + tb), (i >> 1) & 1);
       if (tid == 96) trace_ev(p, 7, i, 2);
       fence_after();
-      float* d = p.dq + ((uint64_t)unit * p.n + q0 + row) * kD;
+      // the dq row goes through the (idle: every dQ MMA of the tile is done)
+      // dS ring as two SW128 fp32 boxes per warp and leaves by TMA store,
+      // instead of 16 scattered 16-byte stores per thread; each warp only
+      // touches its own 32 rows of the staging, and the store has read them
+      // before this warp writes the next tile's dS there
+      const uint32_t stg = sbase + kOffDS;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t r0[32], f[32];
@@ -2586,15 +2591,27 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          float4 v;
-          v.x = (__uint_as_float(r0[4 * k]) + __uint_as_float(f[4 * k])) * p.scale;
-          v.y = (__uint_as_float(r0[4 * k + 1]) + __uint_as_float(f[4 * k + 1])) * p.scale;
-          v.z = (__uint_as_float(r0[4 * k + 2]) + __uint_as_float(f[4 * k + 2])) * p.scale;
-          v.w = (__uint_as_float(r0[4 * k + 3]) + __uint_as_float(f[4 * k + 3])) * p.scale;
-          reinterpret_cast<float4*>(d + 32 * hh)[k] = v;
+          const float v0 = (__uint_as_float(r0[4 * k]) + __uint_as_float(f[4 * k])) * p.scale;
+          const float v1 = (__uint_as_float(r0[4 * k + 1]) + __uint_as_float(f[4 * k + 1])) * p.scale;
+          const float v2 = (__uint_as_float(r0[4 * k + 2]) + __uint_as_float(f[4 * k + 2])) * p.scale;
+          const float v3 = (__uint_as_float(r0[4 * k + 3]) + __uint_as_float(f[4 * k + 3])) * p.scale;
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                           stg + hh * kDSBytes + row * 128 + ((k ^ (row & 7)) << 4)),
+                       "f"(v0), "f"(v1), "f"(v2), "f"(v3));
         }
       }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        const int y = (int)((uint64_t)unit * p.n + q0 + 32 * (warp & 3));
+        tma_store_2d(&m.o, stg + 32 * (warp & 3) * 128, 0, y);
+        tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
+        bulk_commit();
+        bulk_wait_read();
+      }
+      __syncwarp();
     }
+    if (lane == 0) bulk_wait_all();  // dq stores complete before exit
   } else if (warp >= 7) {
     // ------------------------------------------------------------ fine warps
     // fine block of this warp: its 16 rows must be TMEM lanes of the warp's
@@ -3796,6 +3813,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     const uint64_t in_rows = (uint64_t)units * g.n;
     if (llsa_status st = make_tma_map(&maps.q, q, in_rows, kTileQ)) return st;
     if (llsa_status st = make_tma_map(&maps.g, d_out, in_rows, kTileQ)) return st;
+    if (llsa_status st = make_tma_map(&maps.o, P.dq, in_rows, 32, true)) return st;
     const uint64_t tiles = (g.n / kTileQ) * units;
     const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
     tc5_dqf_kernel<<<grid, dqf::kThreads, dqf::kSmem, s>>>(P, maps, units);
