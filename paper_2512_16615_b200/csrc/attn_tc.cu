@@ -1221,10 +1221,16 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   const uint64_t tok_l = p.n / p.pow[level];
   float* gk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl];
   float* gv = gk + (uint64_t)p.cl_split[sl] * tok_l * kD;
-  const uint64_t t = b * kBS + tok;
+  // through smem, so the block's 16 output rows are written row-contiguous
+  __shared__ float4 s_out[2][16][17];
   const float ck = p.cl_ck[sl], cv = p.cl_cv[sl];
-  *reinterpret_cast<float4*>(gk + t * kD + c4) = make_float4(ak.x * ck, ak.y * ck, ak.z * ck, ak.w * ck);
-  *reinterpret_cast<float4*>(gv + t * kD + c4) = make_float4(av.x * cv, av.y * cv, av.z * cv, av.w * cv);
+  s_out[0][tok][c4 / 4] = make_float4(ak.x * ck, ak.y * ck, ak.z * ck, ak.w * ck);
+  s_out[1][tok][c4 / 4] = make_float4(av.x * cv, av.y * cv, av.z * cv, av.w * cv);
+  __syncthreads();
+  const uint32_t orow = threadIdx.x >> 4, ocol = threadIdx.x & 15;
+  const uint64_t t = b * kBS + orow;
+  reinterpret_cast<float4*>(gk + t * kD)[ocol] = s_out[0][orow][ocol];
+  reinterpret_cast<float4*>(gv + t * kD)[ocol] = s_out[1][orow][ocol];
 }
 
 // ---------------------------------------------------------------------------
