@@ -169,7 +169,7 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
 // warp per row extracts the top K by K rounds of a warp arg-max over
 // (score desc, position asc) and emits the kept positions in ascending order.
 template <int CPT>
-__global__ void __launch_bounds__(256) select_level_fast_kernel(
+__global__ void __launch_bounds__(256, 4) select_level_fast_kernel(
     const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
     uint64_t k_unit_stride, const uint32_t* __restrict__ parent, uint64_t parent_unit_stride,
     uint32_t parent_k, uint32_t key_blocks, uint32_t d, uint32_t K, float scale,
@@ -224,31 +224,37 @@ __global__ void __launch_bounds__(256) select_level_fast_kernel(
     const uint32_t r = threadIdx.x >> 4, cg = threadIdx.x & 15;
     // accumulators (s0, s1) and (s2, s3) of each pair as packed fp32x2: the
     // same per-lane operations and order as detail::dot
-    uint64_t acc[CPT][2];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) acc[i][0] = acc[i][1] = 0ull;
+    // two passes of CPT/2 candidates: half the accumulator registers, so
+    // four CTAs fit per SM without spilling
+    constexpr int CH = CPT / 2;
     const ulonglong2* qr = reinterpret_cast<const ulonglong2*>(sq + r * ld);
-    for (uint32_t j = 0; j < d4; ++j) {
-      const ulonglong2 x = qr[j];
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      uint64_t acc[CH][2];
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const uint32_t c = cg + 16 * i;
-        if (c < C) {
-          const ulonglong2 y = reinterpret_cast<const ulonglong2*>(sk + c * ld)[j];
-          acc[i][0] = add2(acc[i][0], mul2_exact(x.x, y.x, negzero2));
-          acc[i][1] = add2(acc[i][1], mul2_exact(x.y, y.y, negzero2));
+      for (int i = 0; i < CH; ++i) acc[i][0] = acc[i][1] = 0ull;
+      for (uint32_t j = 0; j < d4; ++j) {
+        const ulonglong2 x = qr[j];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const uint32_t c = cg + 16 * (pass * CH + i);
+          if (c < C) {
+            const ulonglong2 y = reinterpret_cast<const ulonglong2*>(sk + c * ld)[j];
+            acc[i][0] = add2(acc[i][0], mul2_exact(x.x, y.x, negzero2));
+            acc[i][1] = add2(acc[i][1], mul2_exact(x.y, y.y, negzero2));
+          }
         }
       }
-    }
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const uint32_t c = cg + 16 * i;
-      if (c < C) {
-        const float s0 = __uint_as_float((uint32_t)acc[i][0]);
-        const float s1 = __uint_as_float((uint32_t)(acc[i][0] >> 32));
-        const float s2 = __uint_as_float((uint32_t)acc[i][1]);
-        const float s3 = __uint_as_float((uint32_t)(acc[i][1] >> 32));
-        scores[r * 256 + c] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+      for (int i = 0; i < CH; ++i) {
+        const uint32_t c = cg + 16 * (pass * CH + i);
+        if (c < C) {
+          const float s0 = __uint_as_float((uint32_t)acc[i][0]);
+          const float s1 = __uint_as_float((uint32_t)(acc[i][0] >> 32));
+          const float s2 = __uint_as_float((uint32_t)acc[i][1]);
+          const float s3 = __uint_as_float((uint32_t)(acc[i][1] >> 32));
+          scores[r * 256 + c] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+        }
       }
     }
   }
