@@ -270,6 +270,17 @@ __global__ void segment_order_all_kernel(TrAll a) {
   const uint32_t* seg = a.tmp[l] + u * (uint64_t)a.rows[l] * a.k + s0;
   uint32_t* dst = a.flat[l] + u * a.flat_stride + s0;
   const uint32_t len = s1 - s0;
+  if (len <= 32) {
+    // the whole segment in one register per lane; ranks by shuffles
+    const uint32_t v = lane < len ? seg[lane] : 0xffffffffu;
+    uint32_t rank = 0;
+    for (uint32_t e2 = 0; e2 < len; ++e2) {
+      const uint32_t w = __shfl_sync(0xffffffffu, v, e2);
+      rank += (w < v || (w == v && e2 < lane)) ? 1u : 0u;
+    }
+    if (lane < len) dst[rank] = v;
+    return;
+  }
   for (uint32_t e = lane; e < len; e += 32) {
     const uint32_t v = seg[e];
     uint32_t rank = 0;
