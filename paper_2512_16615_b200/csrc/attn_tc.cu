@@ -2979,7 +2979,9 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     // (a second MMA-issuing thread: the S/dP of chunk c+1 and the accumulate
     // of chunk c are issued concurrently)
     if (lane == 0) {
-      const uint32_t idesc_a = idesc_bf16(128, 64, true, true);
+      // N = 32: B' = [dS | P] (16 + 16 columns); dK^T and dV^T are the two
+      // diagonal 64 x 16 blocks of the 128 x 32 accumulator
+      const uint32_t idesc_a = idesc_bf16(128, 32, true, true);
       uint32_t ai = 0;
       for (uint32_t c = 0;; ++c) {
         const uint32_t s = c % kRing, b = c & 1;
