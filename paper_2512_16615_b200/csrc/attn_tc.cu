@@ -2024,11 +2024,17 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       const uint32_t idesc_o = idesc_bf16(128, kD + 16, false, true);  // O | l_c
       uint32_t vc = 0, pc = 0, i = 0;
       for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
-
-        if (id + gridDim.x < total) {
-          mbar_wait(bar(QEMPTY), i & 1);  // S MMAs of tile i done, fine warps hold Q
-          load_q(id + gridDim.x);
-        }
+        // Q(i+1) may load once tile i's S MMAs are done and the fine warps
+        // hold their Q fragments (QEMPTY); the P·V MMAs of tile i do not read
+        // Q, so that is polled between chunks instead of waited for here
+        bool q_pending = id + gridDim.x < total;
+        auto try_q = [&]() {
+          if (q_pending && mbar_test(bar(QEMPTY), i & 1)) {
+            load_q(id + gridDim.x);
+            q_pending = false;
+          }
+        };
+        try_q();
         const uint32_t ob = i % nob;
         if (i >= nob) mbar_wait(bar(OFREE + ob), ((i / nob) - 1) & 1);
         const uint32_t tO = tmem + o_base + o_stride * ob;
@@ -2048,8 +2054,13 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
           commit(bar(VEMPTY + s));
           commit(bar(PEMPTY + ps));
           trace_ev(p, 3, i, 16 + ch);
+          try_q();
         }
         commit(bar(OREADY + ob));
+        if (q_pending) {
+          mbar_wait(bar(QEMPTY), i & 1);
+          load_q(id + gridDim.x);
+        }
       }
     }
   } else if (warp >= kCoarse0 && warp < kCoarse0 + 8) {

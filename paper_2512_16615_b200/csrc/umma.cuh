@@ -117,6 +117,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
 }
 #endif
 
+// Non-blocking: has the phase with parity `phase` of `mbar` completed?
+__device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(mbar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 // Arrive on `mbar` once every cp.async previously issued by this thread has
 // completed (the arrival does not add to the expected count).
 __device__ __forceinline__ void cp_async_mbar_arrive(uint32_t mbar) {
