@@ -2536,7 +2536,6 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         const uint32_t b = c & 1, ne = ch_info[ch] & 0xFF;
         mbar_wait(bar(SREADY + b), (c >> 1) & 1);
         fence_after();
-        if (c >= 2) mbar_wait(bar(DSFREE + b), ((c >> 1) - 1) & 1);
         const uint32_t sds = sbase + kOffDS + b * kDSBytes;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -2544,6 +2543,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             uint32_t sv[32], gv[32];
             tmem_ld32(tmem + lane_off + b * 128 + 32 * hh, sv);
             tmem_ld32(tmem + lane_off + b * 128 + 64 + 32 * hh, gv);
+            // the dS slot is needed only from the first store on: wait for
+            // it while the TMEM loads are in flight
+            if (hh == 0 && c >= 2) mbar_wait(bar(DSFREE + b), ((c >> 1) - 1) & 1);
             tmem_ld_wait();
             if (2 * hh + 2 >= (int)ne) {  // S / dP all in registers: release the buffer
               fence_before();
