@@ -3395,13 +3395,15 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       uint32_t sv[32], pv[32];
       tmem_ld32(tmem + lane_off + 128 * b + 32 * qh, sv);
       tmem_ld32(tmem + lane_off + 128 * b + 64 + 32 * qh, pv);
+      // the P^T / dS^T slot is needed only for the stores: wait for it while
+      // the TMEM loads are in flight
+      if (t >= 2) mbar_wait(bar(PFREE + b), ((t >> 1) - 1) & 1);
       tmem_ld_wait();
       fence_before();
       mbar_arrive(bar(SFREE + b));
       const float* lse = reinterpret_cast<const float*>(smem + Lay::kOffQ + s * kQStage +
                                                         2 * kQT * 128) + 32 * qh;
       const float* Dq = lse + kQT;
-      if (t >= 2) mbar_wait(bar(PFREE + b), ((t >> 1) - 1) & 1);
       const uint32_t sPT = sbase + Lay::kOffP + b * 32768, sDST = sPT + 16384;
 #pragma unroll
       for (int c8 = 0; c8 < 4; ++c8) {
