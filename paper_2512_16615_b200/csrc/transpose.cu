@@ -259,36 +259,45 @@ __global__ void scatter_all_kernel(TrAll a) {
   }
 }
 
+// One 8-lane group per key block (four blocks per warp): segments of up to 8
+// entries are ranked with group shuffles, longer ones by the group's lanes
+// scanning the segment.
 __global__ void segment_order_all_kernel(TrAll a) {
   const uint32_t l = blockIdx.y;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (warp >= (uint64_t)a.kb[l] * a.units) return;
-  const uint64_t u = warp / a.kb[l], b = warp - u * a.kb[l];
-  const uint32_t* off = a.offs[l] + u * a.off_stride;
-  const uint32_t s0 = off[b], s1 = off[b + 1];
-  const uint32_t* seg = a.tmp[l] + u * (uint64_t)a.rows[l] * a.k + s0;
-  uint32_t* dst = a.flat[l] + u * a.flat_stride + s0;
-  const uint32_t len = s1 - s0;
-  if (len <= 32) {
-    // the whole segment in one register per lane; ranks by shuffles
-    const uint32_t v = lane < len ? seg[lane] : 0xffffffffu;
-    uint32_t rank = 0;
-    for (uint32_t e2 = 0; e2 < len; ++e2) {
-      const uint32_t w = __shfl_sync(0xffffffffu, v, e2);
-      rank += (w < v || (w == v && e2 < lane)) ? 1u : 0u;
-    }
-    if (lane < len) dst[rank] = v;
-    return;
+  const uint64_t grp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3;
+  const uint32_t sl = threadIdx.x & 7;
+  const uint64_t nb = (uint64_t)a.kb[l] * a.units;
+  const bool live = grp < nb;
+  uint32_t len = 0, s0 = 0;
+  const uint32_t* seg = nullptr;
+  uint32_t* dst = nullptr;
+  if (live) {
+    const uint64_t u = grp / a.kb[l], b = grp - u * a.kb[l];
+    const uint32_t* off = a.offs[l] + u * a.off_stride;
+    s0 = off[b];
+    len = off[b + 1] - s0;
+    seg = a.tmp[l] + u * (uint64_t)a.rows[l] * a.k + s0;
+    dst = a.flat[l] + u * a.flat_stride + s0;
   }
-  for (uint32_t e = lane; e < len; e += 32) {
-    const uint32_t v = seg[e];
-    uint32_t rank = 0;
+  // the group's 8 lanes share len, so the branch below is group-uniform;
+  // shuffles run over the whole warp with width 8
+  const bool small = len <= 8;
+  const uint32_t v = (live && small && sl < len) ? seg[sl] : 0xffffffffu;
+  uint32_t rank = 0;
+  for (uint32_t e2 = 0; e2 < 8; ++e2) {
+    const uint32_t w = __shfl_sync(0xffffffffu, v, e2, 8);
+    rank += (e2 < len && (w < v || (w == v && e2 < sl))) ? 1u : 0u;
+  }
+  if (live && small && sl < len) dst[rank] = v;
+  if (!live || small) return;
+  for (uint32_t e = sl; e < len; e += 8) {
+    const uint32_t x = seg[e];
+    uint32_t r = 0;
     for (uint32_t e2 = 0; e2 < len; ++e2) {
       const uint32_t w = seg[e2];
-      rank += (w < v || (w == v && e2 < e)) ? 1u : 0u;
+      r += (w < x || (w == x && e2 < e)) ? 1u : 0u;
     }
-    dst[rank] = v;
+    dst[r] = x;
   }
 }
 
@@ -346,8 +355,8 @@ llsa_status transpose_all_fused(const Geometry& g, uint32_t units, const uint32_
   scatter_all_kernel<<<ge, 256, 0, s>>>(a);
   count_launch();
   LLSA_LAUNCH_CHECK("scatter_all_kernel");
-  const uint64_t warps = maxkb * units;
-  segment_order_all_kernel<<<dim3((unsigned)((warps * 32 + 255) / 256), g.L), 256, 0, s>>>(a);
+  const uint64_t groups = maxkb * units;  // 8 lanes per key block
+  segment_order_all_kernel<<<dim3((unsigned)((groups * 8 + 255) / 256), g.L), 256, 0, s>>>(a);
   count_launch();
   LLSA_LAUNCH_CHECK("segment_order_all_kernel");
   return LLSA_OK;
