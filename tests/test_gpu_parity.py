@@ -305,12 +305,18 @@ def test_handle_path_matches_oracle(oracle_c, cfg, bf):
 # staged SIMT path (fp32 math, itself pinned to the oracle above) on the same
 # bf16 inputs: tables bit-exact, outputs and gradients within the bf16 bar.
 # K = 16 gives 33 coarse entries, past the tcgen05 forward / dQ kernels'
-# 24-entry TMEM budget, so it runs their mma.sync fallbacks.
+# 24-entry TMEM budget, so it runs their mma.sync fallbacks.  The C5 cases
+# (N = 262144; L = 4 is inadmissible there, so L = 3) cover
+# K = 4 / 16 with full enrichment and L_e = 0 (fine blocks only).
 @pytest.mark.parametrize("cfg", [Config(65536, 64, 16, 8, 3, 3),
                                  Config(65536, 64, 16, 16, 3, 3),
                                  Config(65536, 64, 16, 8, 3, 1),
-                                 Config(65536, 64, 16, 8, 3, 3, reweight_mode=1)],
-                         ids=["C3", "C3-K16", "C3-Le1", "C3-LogitBias"])
+                                 Config(65536, 64, 16, 8, 3, 3, reweight_mode=1),
+                                 Config(262144, 64, 16, 4, 3, 3),
+                                 Config(262144, 64, 16, 16, 3, 3),
+                                 Config(262144, 64, 16, 8, 3, 0)],
+                         ids=["C3", "C3-K16", "C3-Le1", "C3-LogitBias", "C5-K4", "C5-K16",
+                              "C5-Le0"])
 def test_full_size_tensor_core_path_matches_simt(cfg):
     g = torch.Generator(device="cuda").manual_seed(7)
     q, k, v, dO = (torch.randn(1, cfg.n, 64, device="cuda", generator=g).to(torch.bfloat16)
