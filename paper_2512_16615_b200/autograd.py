@@ -71,4 +71,11 @@ class LLSAAttention(torch.nn.Module):
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor) -> torch.Tensor:
         if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
             raise ValueError("q, k, v must share shape [batch, heads, n, d]")
+        if tuple(q.shape[-2:]) != (self.cfg.n, self.cfg.d):
+            raise ValueError(f"q, k, v must be [batch, heads, {self.cfg.n}, {self.cfg.d}] for "
+                             f"this layer, got {tuple(q.shape)}")
+        if q.dtype not in (torch.bfloat16, torch.float32) or k.dtype != q.dtype or \
+                v.dtype != q.dtype:
+            raise ValueError("q, k, v must all be bfloat16 or all float32 "
+                             f"(got {q.dtype}, {k.dtype}, {v.dtype})")
         return _LLSAFunction.apply(q, k, v, self)

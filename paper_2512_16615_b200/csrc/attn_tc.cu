@@ -29,6 +29,7 @@
 //     pooling adjoint of every coarse level and writes dk, dv once.
 #include <cuda.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <type_traits>
@@ -3677,15 +3678,34 @@ static llsa_status make_tma_map(CUtensorMap* map, const void* base, uint64_t row
   return LLSA_OK;
 }
 
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 ? 0 : dev;
+}
+
+// SM count of the current device (cached per device; a process may drive
+// several GPUs, one handle each).
 static int num_sms() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  const int dev = current_device() & 63;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+// Kernel attributes (the >48 KB dynamic shared memory opt-ins) are per device
+// context: one "done" bit per device.  Two threads racing on the same device
+// both set the attributes, which is harmless.
+static bool attrs_done(const std::atomic<uint64_t>& mask) {
+  return (mask.load(std::memory_order_acquire) >> (current_device() & 63)) & 1;
+}
+static void mark_attrs_done(std::atomic<uint64_t>& mask) {
+  mask.fetch_or(1ull << (current_device() & 63), std::memory_order_release);
 }
 
 static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* pk,
@@ -3722,13 +3742,13 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
   P.out = out;
   P.row_max = row_max;
   P.row_denom = row_denom;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!attrs_done(attr)) {
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFwdSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc5_fwd_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, fw5::kSmem));
-    attr = true;
+    mark_attrs_done(attr);
   }
   if (fwd5_path(g)) {
     TmaMaps maps{};
@@ -3795,8 +3815,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   P.dq = dq;
   P.dk = dk;
   P.dv = dv;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (!attrs_done(attr)) {
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kDqSmem));
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<2>,
@@ -3828,7 +3848,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_kv_kernel<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        KvCfg<false>::Smem));
-    attr = true;
+    mark_attrs_done(attr);
   }
   const bool dqf = dqf_path(g);
   if (dqf) {

@@ -701,6 +701,18 @@ struct llsa_handle_s {
   size_t sizes[8] = {};
 };
 
+// The handle's kernels run on the device it was created on, whatever device
+// is current in the calling thread; the caller's current device is restored.
+struct DeviceGuard {
+  int prev = -1, want;
+  explicit DeviceGuard(int dev) : want(dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != want) cudaSetDevice(want);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+  }
+};
+
 llsa_status llsa_handle_create(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
                                llsa_handle* out) {
   NONNULL(out);
@@ -769,6 +781,7 @@ int llsa_handle_uses_tensor_cores(llsa_handle h) { return h && h->tc ? 1 : 0; }
 llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, const void* v,
                                 float* out, void* stream) {
   NONNULL(h);
+  DeviceGuard dg(h->device);
   NONNULL(q);
   NONNULL(k);
   NONNULL(v);
@@ -810,6 +823,7 @@ llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q
                                  const void* k, const void* v, const float* out, float* dq,
                                  float* dk, float* dv, void* stream) {
   NONNULL(h);
+  DeviceGuard dg(h->device);
   NONNULL(d_out);
   NONNULL(q);
   NONNULL(k);

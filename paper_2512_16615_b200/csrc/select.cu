@@ -8,8 +8,10 @@
 // (selection.cpp:21-38) with its lowest-index tie-break, computed without a
 // sort and with float comparisons (−0.0 ties +0.0).  Kept candidates are
 // emitted in ascending position order; candidate ids ascend with position
-// (parent rows are sorted), so rows come out ascending as the reference's
-// final std::sort makes them.
+// when the parent row is sorted (always, on the hierarchical path), so rows
+// come out ascending as the reference's final std::sort makes them.  A
+// user-supplied parent row that is not ascending is detected per CTA and the
+// kept ids are then sorted explicitly (selection.cpp:37).
 //
 // select_level: one CTA per (unit, level-l query block).  All B query rows
 // of the block share the same K·B candidate tokens, so the CTA stages those
@@ -22,6 +24,14 @@ namespace llsa_impl {
 namespace {
 
 using namespace llsa_dev;
+
+// true when this thread's slice of a parent row is strictly ascending (the
+// hierarchical path always produces such rows; ids then ascend with position)
+__device__ __forceinline__ bool row_ascending(const uint32_t* prow, uint32_t parent_k) {
+  bool ok = true;
+  for (uint32_t t = threadIdx.x; t + 1 < parent_k; t += blockDim.x) ok &= prow[t] < prow[t + 1];
+  return ok;
+}
 
 __device__ __forceinline__ bool beats(float sa, uint32_t a, float sb, uint32_t b) {
   // true when candidate a ranks before candidate b
@@ -103,7 +113,7 @@ __global__ void __launch_bounds__(256) select_level_kernel(
   const float* qu = q + unit * q_unit_stride + (uint64_t)blk * B * d;
   for (uint32_t e = threadIdx.x; e < B * d; e += blockDim.x)
     sq[(e / d) * ld + e % d] = qu[e];
-  __syncthreads();
+  const bool asc = __syncthreads_and(row_ascending(prow, parent_k)) != 0;
   const float* ku = k + unit * k_unit_stride;
   if (stage_k) {
     for (uint64_t e = threadIdx.x; e < (uint64_t)C * d; e += blockDim.x) {
@@ -143,6 +153,18 @@ __global__ void __launch_bounds__(256) select_level_kernel(
     uint32_t pos = 0;
     for (uint32_t c2 = 0; c2 < c; ++c2) pos += sr[c2];
     o[(uint64_t)r * K + pos] = ids[c];
+  }
+  if (!asc) {  // a user-built parent row out of order: sort like topk_row's std::sort
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < B; r += blockDim.x) {
+      uint32_t* orow = o + (uint64_t)r * K;
+      for (uint32_t i = 1; i < K; ++i) {
+        const uint32_t x = orow[i];
+        uint32_t j = i;
+        for (; j > 0 && orow[j - 1] > x; --j) orow[j] = orow[j - 1];
+        orow[j] = x;
+      }
+    }
   }
 }
 
@@ -206,7 +228,7 @@ __global__ void __launch_bounds__(256, 4) select_level_fast_kernel(
     rc(e, r, j);
     reinterpret_cast<float4*>(sq + r * ld)[j] = reinterpret_cast<const float4*>(qu + r * d)[j];
   }
-  __syncthreads();
+  const bool asc = __syncthreads_and(row_ascending(prow, parent_k)) != 0;
   // candidate rows: global → smem with cp.async (no register round trip, so
   // a thread's copies are all in flight at once)
   const float* ku = k + unit * k_unit_stride;
@@ -308,6 +330,17 @@ __global__ void __launch_bounds__(256, 4) select_level_fast_kernel(
 #pragma unroll
     for (int i = 0; i < PL; ++i)
       if ((taken >> i) & 1u) o[pos++] = ids[lane * PL + i];
+    if (!asc) {  // parent row out of order (user-built): rank-sort the K ids
+      __syncwarp();
+      const uint32_t x = lane < K ? o[lane] : 0u;
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < K; ++j) {
+        const uint32_t y = __shfl_sync(0xffffffffu, x, j);
+        rank += (y < x || (y == x && j < lane)) ? 1u : 0u;
+      }
+      __syncwarp();
+      if (lane < K) o[rank] = x;
+    }
   }
 }
 

@@ -93,31 +93,97 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ idx, uint64_t idx_un
   }
 }
 
-// One warp per (unit, key block): out[off + rank(e)] = tmp[e].
-__global__ void segment_order_kernel(const uint32_t* __restrict__ tmp,
-                                     uint64_t tmp_unit_stride,
-                                     const uint32_t* __restrict__ offsets,
-                                     uint64_t off_unit_stride, uint32_t key_blocks,
-                                     uint32_t units, uint32_t* __restrict__ flat,
-                                     uint64_t flat_unit_stride) {
+// Long segments (hot key blocks picked by many query blocks: up to T entries)
+// would make the per-element rank scan O(len²); a CTA instead sorts them
+// cooperatively.  Kernels collect their long segments in a shared list and,
+// after a barrier, the whole CTA sorts each one with a bitonic network in the
+// "flip" formulation (every compare-exchange puts the minimum at the lower
+// index), which lets the sequence stay unpadded: a partner index ≥ len is a
+// virtual +inf and its comparison is a no-op.  Row ids are plain integers,
+// so no stability question arises.  O(len log² len) per segment.
+constexpr uint32_t kLongSeg = 64;     // longer segments take the CTA sort
+constexpr uint32_t kSortSmem = 4096;  // sorted in shared memory up to this length
+
+struct LongSeg {
+  const uint32_t* src;
+  uint32_t* dst;
+  uint32_t len;
+};
+
+__device__ __forceinline__ void cx(uint32_t* a, uint32_t i, uint32_t j) {
+  const uint32_t x = a[i], y = a[j];
+  if (y < x) {
+    a[i] = y;
+    a[j] = x;
+  }
+}
+
+// whole-CTA sort of src[0..len) into dst (may run in place over dst)
+__device__ void cta_sort_segment(const uint32_t* src, uint32_t* dst, uint32_t len,
+                                 uint32_t* sbuf) {
+  const bool in_smem = len <= kSortSmem;
+  uint32_t* a = in_smem ? sbuf : dst;
+  for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) a[e] = src[e];
+  __syncthreads();
+  for (uint32_t k = 2; k < 2 * len; k <<= 1) {
+    // flip step: i ↔ i ^ (k - 1) within each k-block
+    for (uint32_t t = threadIdx.x; t < (len + 1) / 2 + k; t += blockDim.x) {
+      const uint32_t blk = t / (k / 2), off = t % (k / 2);
+      const uint32_t i = blk * k + off, j = blk * k + (k - 1 - off);
+      if (j < len) cx(a, i, j);
+    }
+    __syncthreads();
+    for (uint32_t h = k / 4; h >= 1; h >>= 1) {  // half-cleaners
+      for (uint32_t t = threadIdx.x; t < (len + 1) / 2 + h; t += blockDim.x) {
+        const uint32_t blk = t / h, off = t % h;
+        const uint32_t i = blk * 2 * h + off, j = i + h;
+        if (j < len) cx(a, i, j);
+      }
+      __syncthreads();
+    }
+  }
+  if (in_smem) {
+    for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) dst[e] = a[e];
+    __syncthreads();
+  }
+}
+
+// One warp per (unit, key block): out[off + rank(e)] = tmp[e]; segments past
+// kLongSeg entries take the CTA sort.
+__global__ void __launch_bounds__(256) segment_order_kernel(
+    const uint32_t* __restrict__ tmp, uint64_t tmp_unit_stride,
+    const uint32_t* __restrict__ offsets, uint64_t off_unit_stride, uint32_t key_blocks,
+    uint32_t units, uint32_t* __restrict__ flat, uint64_t flat_unit_stride) {
+  __shared__ LongSeg longs[8];
+  __shared__ uint32_t nlong;
+  __shared__ uint32_t sbuf[kSortSmem];
+  if (threadIdx.x == 0) nlong = 0;
+  __syncthreads();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  if (warp >= (uint64_t)key_blocks * units) return;
-  const uint64_t u = warp / key_blocks, b = warp - u * key_blocks;
-  const uint32_t* off = offsets + u * off_unit_stride;
-  const uint32_t s0 = off[b], s1 = off[b + 1];
-  const uint32_t* seg = tmp + u * tmp_unit_stride + s0;
-  uint32_t* dst = flat + u * flat_unit_stride + s0;
-  const uint32_t len = s1 - s0;
-  for (uint32_t e = lane; e < len; e += 32) {
-    const uint32_t v = seg[e];
-    uint32_t rank = 0;
-    for (uint32_t e2 = 0; e2 < len; ++e2) {
-      const uint32_t w = seg[e2];
-      rank += (w < v || (w == v && e2 < e)) ? 1u : 0u;
+  if (warp < (uint64_t)key_blocks * units) {
+    const uint64_t u = warp / key_blocks, b = warp - u * key_blocks;
+    const uint32_t* off = offsets + u * off_unit_stride;
+    const uint32_t s0 = off[b], s1 = off[b + 1];
+    const uint32_t* seg = tmp + u * tmp_unit_stride + s0;
+    uint32_t* dst = flat + u * flat_unit_stride + s0;
+    const uint32_t len = s1 - s0;
+    if (len > kLongSeg) {
+      if (lane == 0) longs[atomicAdd(&nlong, 1u)] = LongSeg{seg, dst, len};
+    } else {
+      for (uint32_t e = lane; e < len; e += 32) {
+        const uint32_t v = seg[e];
+        uint32_t rank = 0;
+        for (uint32_t e2 = 0; e2 < len; ++e2) {
+          const uint32_t w = seg[e2];
+          rank += (w < v || (w == v && e2 < e)) ? 1u : 0u;
+        }
+        dst[rank] = v;
+      }
     }
-    dst[rank] = v;
   }
+  __syncthreads();
+  for (uint32_t i = 0; i < nlong; ++i) cta_sort_segment(longs[i].src, longs[i].dst, longs[i].len, sbuf);
 }
 
 unsigned grid_for(uint64_t threads, int block) {
@@ -260,9 +326,14 @@ __global__ void scatter_all_kernel(TrAll a) {
 }
 
 // One 8-lane group per key block (four blocks per warp): segments of up to 8
-// entries are ranked with group shuffles, longer ones by the group's lanes
-// scanning the segment.
-__global__ void segment_order_all_kernel(TrAll a) {
+// entries are ranked with group shuffles, up to kLongSeg by the group's lanes
+// scanning the segment, longer ones by the CTA sort.
+__global__ void __launch_bounds__(256) segment_order_all_kernel(TrAll a) {
+  __shared__ LongSeg longs[32];
+  __shared__ uint32_t nlong;
+  __shared__ uint32_t sbuf[kSortSmem];
+  if (threadIdx.x == 0) nlong = 0;
+  __syncthreads();
   const uint32_t l = blockIdx.y;
   const uint64_t grp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 3;
   const uint32_t sl = threadIdx.x & 7;
@@ -279,7 +350,7 @@ __global__ void segment_order_all_kernel(TrAll a) {
     seg = a.tmp[l] + u * (uint64_t)a.rows[l] * a.k + s0;
     dst = a.flat[l] + u * a.flat_stride + s0;
   }
-  // the group's 8 lanes share len, so the branch below is group-uniform;
+  // the group's 8 lanes share len, so the branches below are group-uniform;
   // shuffles run over the whole warp with width 8
   const bool small = len <= 8;
   const uint32_t v = (live && small && sl < len) ? seg[sl] : 0xffffffffu;
@@ -289,16 +360,21 @@ __global__ void segment_order_all_kernel(TrAll a) {
     rank += (e2 < len && (w < v || (w == v && e2 < sl))) ? 1u : 0u;
   }
   if (live && small && sl < len) dst[rank] = v;
-  if (!live || small) return;
-  for (uint32_t e = sl; e < len; e += 8) {
-    const uint32_t x = seg[e];
-    uint32_t r = 0;
-    for (uint32_t e2 = 0; e2 < len; ++e2) {
-      const uint32_t w = seg[e2];
-      r += (w < x || (w == x && e2 < e)) ? 1u : 0u;
+  if (live && !small && len <= kLongSeg) {
+    for (uint32_t e = sl; e < len; e += 8) {
+      const uint32_t x = seg[e];
+      uint32_t r = 0;
+      for (uint32_t e2 = 0; e2 < len; ++e2) {
+        const uint32_t w = seg[e2];
+        r += (w < x || (w == x && e2 < e)) ? 1u : 0u;
+      }
+      dst[r] = x;
     }
-    dst[r] = x;
+  } else if (live && len > kLongSeg && sl == 0) {
+    longs[atomicAdd(&nlong, 1u)] = LongSeg{seg, dst, len};
   }
+  __syncthreads();
+  for (uint32_t i = 0; i < nlong; ++i) cta_sort_segment(longs[i].src, longs[i].dst, longs[i].len, sbuf);
 }
 
 }  // namespace

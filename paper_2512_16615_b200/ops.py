@@ -498,6 +498,10 @@ class LLSAHandle:
                  dtype: torch.dtype = torch.bfloat16, device: int | None = None):
         self.lib = _lib.load()
         self.cfg = cfg if isinstance(cfg, ValidatedConfig) else validate_config(cfg)
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise _lib.ArgumentError(f"LLSAHandle dtype must be bfloat16 or float32, got {dtype}")
+        if units < 1:
+            raise _lib.ArgumentError("LLSAHandle needs at least one unit")
         self.units = units
         self.dtype = dtype
         dev = torch.cuda.current_device() if device is None else device
@@ -557,22 +561,52 @@ class LLSAHandle:
         t = _from_ptr(p, numel, dt, self.device)
         return t.view(shape)
 
+    def _check_inputs(self, **ts) -> None:
+        """Every tensor handed to the C ABI must be [units, n, d] of the
+        handle's dtype on the handle's device (the C entry points take raw
+        pointers and cannot check sizes themselves)."""
+        shape = (self.units, self.cfg.n, self.cfg.d)
+        for name, t in ts.items():
+            if tuple(t.shape) != shape:
+                raise _lib.ShapeMismatch(f"{name} has shape {tuple(t.shape)}, the handle "
+                                         f"expects {shape}")
+            if t.dtype != self.dtype:
+                raise _lib.ArgumentError(f"{name} is {t.dtype}, the handle was built for "
+                                         f"{self.dtype}")
+            if t.device != self.device:
+                raise _lib.ArgumentError(f"{name} is on {t.device}, the handle on {self.device}")
+
+    def _check_outputs(self, **ts) -> None:
+        shape = (self.units, self.cfg.n, self.cfg.d)
+        for name, t in ts.items():
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or \
+                    t.device != self.device or not t.is_contiguous():
+                raise _lib.ShapeMismatch(f"{name} must be a contiguous float32 {shape} tensor "
+                                         f"on {self.device}")
+
     def forward(self, q, k, v, out=None):
+        self._check_inputs(q=q, k=k, v=v)
         q, k, v = (t.contiguous() for t in (q, k, v))
         out = out if out is not None else torch.empty(q.shape, device=q.device,
                                                       dtype=torch.float32)
-        check(self.lib.llsa_handle_forward(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
-                                           _stream()))
+        self._check_outputs(out=out)
+        with torch.cuda.device(self.device):
+            check(self.lib.llsa_handle_forward(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                               _stream()))
         return out
 
     def backward(self, d_out, q, k, v, out, dq=None, dk=None, dv=None):
+        self._check_inputs(d_out=d_out, q=q, k=k, v=v)
         d_out, q, k, v = (t.contiguous() for t in (d_out, q, k, v))
         mk = lambda: torch.empty(q.shape, device=q.device, dtype=torch.float32)  # noqa: E731
         dq = dq if dq is not None else mk()
         dk = dk if dk is not None else mk()
         dv = dv if dv is not None else mk()
-        check(self.lib.llsa_handle_backward(self._h, _ptr(d_out), _ptr(q), _ptr(k), _ptr(v),
-                                            _ptr(out), _ptr(dq), _ptr(dk), _ptr(dv), _stream()))
+        self._check_outputs(out=out, dq=dq, dk=dk, dv=dv)
+        with torch.cuda.device(self.device):
+            check(self.lib.llsa_handle_backward(self._h, _ptr(d_out), _ptr(q), _ptr(k), _ptr(v),
+                                                _ptr(out), _ptr(dq), _ptr(dk), _ptr(dv),
+                                                _stream()))
         return dq, dk, dv
 
 

@@ -111,6 +111,22 @@ def test_select_level_bit_exact_and_validation(oracle_c):
         llsa.sync_status()
 
 
+def test_select_level_unsorted_parent_rows_match_oracle(oracle_c):
+    # topk_row ends with std::sort (selection.cpp:37): the output rows ascend
+    # whatever order the parent row lists its blocks in.  d = 64, B = 16 runs
+    # the fast kernel; d = 4, B = 4 the generic one.
+    rng = np.random.default_rng(5)
+    for rows, d, b, k in ((4096, 64, 16, 8), (64, 4, 4, 3)):
+        kb = rows // b
+        q = oracle_c.gen_random(rows, d, 50)
+        kk = oracle_c.gen_random(rows, d, 51)
+        parent = np.stack([rng.permutation(kb)[:k] for _ in range(rows // b)]).astype(np.uint32)
+        got = llsa.select_level(T(q), T(kk), T(parent, torch.int32), 1, k, 0.125, b)
+        want = oracle_c.select_level(q, kk, parent, 1, k, 0.125, b)
+        np.testing.assert_array_equal(U32(got[0]), want)
+        assert (np.diff(U32(got[0]).astype(np.int64), axis=1) > 0).all()
+
+
 @pytest.mark.parametrize("name", ["c1_n4096_L1", "c1_n4096_L2", "c2_n16384_L2",
                                   "c3_n65536_L3", "c3p_n65536_L2"])
 def test_hierarchical_topk_matches_reference_tables(golden, oracle_c, name):
@@ -169,6 +185,42 @@ def test_transpose_degenerate_long_segment(oracle_c):
     wo, wf = oracle_c.transpose(idx, 4096)
     np.testing.assert_array_equal(U32(o[0]), wo)
     np.testing.assert_array_equal(U32(f[0]), wf)
+
+
+def test_handle_skewed_selection_long_segments(oracle_c):
+    # constant keys: every score of a row ties, so every query block picks the
+    # K lowest blocks (topk_row's tie-break) and each picked key block's CSC
+    # segment holds every query block of its level (4096/256/16 entries at
+    # N = 65536, L = 3): the transpose's CTA-sort path, then the backward
+    # walks those hot segments
+    cfg = Config(16384, 64, 16, 8, 2, 2)
+    q, _, v, dO = unit_inputs(cfg, 0, bf16=True, backend=oracle_c)
+    k = np.full_like(q, 0.5)
+    ref = oracle_c.run(cfg, q, k, v, dO)
+    h = llsa.LLSAHandle(llsa.LLSAConfig(cfg.n, 64, 16, 8, 2, 2), 1, torch.bfloat16)
+    tq, tk, tv, tdo = (T(a, torch.bfloat16)[None] for a in (q, k, v, dO))
+    out = h.forward(tq, tk, tv)
+    dq, dk, dv = h.backward(tdo, tq, tk, tv, out)
+    llsa.sync_status()
+    np.testing.assert_array_equal(U32(h.view("tables"))[0], ref.tables)
+    np.testing.assert_array_equal(U32(h.view("csc_offsets"))[0], ref.csc_offsets)
+    np.testing.assert_array_equal(U32(h.view("csc_flat"))[0], ref.csc_flat)
+    for name, got, want in (("out", out, ref.out), ("dq", dq, ref.dq), ("dk", dk, ref.dk),
+                            ("dv", dv, ref.dv)):
+        e = rel_err(got[0].cpu().numpy(), want)
+        assert e["max_rel"] <= 2e-2, (name, e)
+    # and at N = 65536 through the transpose alone (segments up to 4096 long)
+    cfg3 = Config(65536, 64, 16, 8, 3, 3)
+    vc = vcfg(cfg3)
+    tables = np.concatenate([np.tile(np.arange(8, dtype=np.int32), rows)
+                             for rows in cfg3.table_rows()])
+    offs, flat = llsa.transpose_all(T(tables, torch.int32)[None], vc)
+    for l, t in enumerate(cfg3.split_tables(tables.astype(np.uint32))):
+        wo, wf = oracle_c.transpose(t, cfg3.level_blocks(l))
+        lo = sum(cfg3.level_blocks(j) + 1 for j in range(l))
+        lf = sum(cfg3.level_blocks(j) * 8 for j in range(l))
+        np.testing.assert_array_equal(U32(offs[0])[lo:lo + wo.size], wo)
+        np.testing.assert_array_equal(U32(flat[0])[lf:lf + wf.size], wf)
 
 
 def test_transpose_out_of_range_flags():
@@ -266,11 +318,16 @@ def test_zero_cotangent_gives_zero_gradients(oracle_c):
                                     (Config(16384, 64, 16, 8, 2, 2, reweight_mode=1), True),
                                     (Config(16384, 64, 16, 8, 2, 0), True),
                                     (Config(65536, 64, 16, 8, 3, 3), True)])
-def test_handle_path_matches_oracle(oracle_c, cfg, bf):
+def test_handle_path_matches_oracle(oracle_c, reference, cfg, bf):
+    # the single-threaded C restatement up to C2; the multi-threaded compiled
+    # reference at N = 65536 (forward and backward on both units)
     units = 2
-    ins = [unit_inputs(cfg, u, bf16=bf, backend=oracle_c) for u in range(units)]
-    want_bwd = cfg.n <= 16384
-    refs = [oracle_c.run(cfg, q, k, v, dO if want_bwd else None) for q, k, v, dO in ins]
+    import os
+    reference.set_threads(os.cpu_count() or 1)
+    be = oracle_c if cfg.n <= 16384 else reference
+    ins = [unit_inputs(cfg, u, bf16=bf, backend=be) for u in range(units)]
+    want_bwd = True
+    refs = [be.run(cfg, q, k, v, dO) for q, k, v, dO in ins]
     dt = torch.bfloat16 if bf else torch.float32
     q, k, v, dO = (T(np.stack([i[j] for i in ins]), dt) for j in range(4))
     h = llsa.LLSAHandle(llsa.LLSAConfig(cfg.n, cfg.d, cfg.block_size, cfg.top_k, cfg.levels,
@@ -282,7 +339,10 @@ def test_handle_path_matches_oracle(oracle_c, cfg, bf):
     for u in range(units):
         np.testing.assert_array_equal(tables[u], refs[u].tables)
         e = rel_err(out[u].cpu().numpy(), refs[u].out)
-        assert e["max_rel"] <= tol, ("out", u, e)
+        assert e["max_rel"] <= tol and e["worst_row"] <= 2.5 * tol, ("out", u, e)
+        g_lse = lse(h.view("row_max")[u].cpu().numpy(), h.view("row_denom")[u].cpu().numpy())
+        assert np.abs(g_lse - lse(refs[u].row_max, refs[u].row_denom)).max() <= \
+            (5e-3 if bf else 1e-4)
     if want_bwd:
         dq, dk, dv = h.backward(dO, q, k, v, out)
         llsa.sync_status()
@@ -290,7 +350,7 @@ def test_handle_path_matches_oracle(oracle_c, cfg, bf):
             for name, got, want in (("dq", dq, refs[u].dq), ("dk", dk, refs[u].dk),
                                     ("dv", dv, refs[u].dv)):
                 e = rel_err(got[u].cpu().numpy(), want)
-                assert e["max_rel"] <= tol, (name, u, e)
+                assert e["max_rel"] <= tol and e["worst_row"] <= 2.5 * tol, (name, u, e)
         # determinism: a second run is bitwise identical
         out2 = h.forward(q, k, v)
         g2 = h.backward(dO, q, k, v, out2)
@@ -299,48 +359,85 @@ def test_handle_path_matches_oracle(oracle_c, cfg, bf):
             assert torch.equal(a, b)
 
 
-# ------------------------------------------- full-size tcgen05 path vs SIMT path
-# The L = 3 backward (B = 16 needs N >= 65536) is beyond what the C oracle
-# runs in test time, so the tensor-core handle path is checked against the
-# staged SIMT path (fp32 math, itself pinned to the oracle above) on the same
-# bf16 inputs: tables bit-exact, outputs and gradients within the bf16 bar.
-# K = 16 gives 33 coarse entries, past the tcgen05 forward / dQ kernels'
-# 24-entry TMEM budget, so it runs their mma.sync fallbacks.  The C5 cases
-# (N = 262144; L = 4 is inadmissible there, so L = 3) cover
-# K = 4 / 16 with full enrichment and L_e = 0 (fine blocks only).
-@pytest.mark.parametrize("cfg", [Config(65536, 64, 16, 8, 3, 3),
-                                 Config(65536, 64, 16, 16, 3, 3),
-                                 Config(65536, 64, 16, 8, 3, 1),
-                                 Config(65536, 64, 16, 8, 3, 3, reweight_mode=1),
-                                 Config(262144, 64, 16, 4, 3, 3),
-                                 Config(262144, 64, 16, 16, 3, 3),
-                                 Config(262144, 64, 16, 8, 3, 0)],
-                         ids=["C3", "C3-K16", "C3-Le1", "C3-LogitBias", "C5-K4", "C5-K16",
-                              "C5-Le0"])
-def test_full_size_tensor_core_path_matches_simt(cfg):
-    g = torch.Generator(device="cuda").manual_seed(7)
-    q, k, v, dO = (torch.randn(1, cfg.n, 64, device="cuda", generator=g).to(torch.bfloat16)
-                   for _ in range(4))
+# ------------------------------------- full-size tcgen05 path vs the reference
+# The compiled, unmodified reference (oracle/_ref/libllsa_ref32.so, the f32
+# build, multi-threaded) is the checker at every BASELINE size: C2, C3 (K = 8
+# and 16, L_e = 3 and 1, ScaleKV and LogitBias), C3' (L = 2) and all six C5
+# points (N = 262144, K = 4 / 8 / 16, L_e = 3 and 0; L = 4 is inadmissible at
+# N = 262144).  Inputs are the reference's own gen_random
+# streams rounded to bf16; the reference runs on the same
+# widened values.  Bars: every selection table bit-exact; O, dq, dk, dv within
+# 2e-2 of max|ref| AND 1e-2 relative Frobenius AND 5e-2 worst-row relative
+# (a missing or mis-weighted coarse contribution in a low-magnitude row shows
+# up in the last two); the LSE m + ln(denom) from the handle's row_max /
+# row_denom within 5e-3 absolute.  The measured errors are appended to
+# $LLSA_PARITY_LOG (profiles/r2_parity.json keeps a round's run).
+REF_CASES = [
+    ("C2", Config(16384, 64, 16, 8, 2, 2)),
+    ("C3", Config(65536, 64, 16, 8, 3, 3)),
+    ("C3-K16", Config(65536, 64, 16, 16, 3, 3)),
+    ("C3-Le1", Config(65536, 64, 16, 8, 3, 1)),
+    ("C3-LogitBias", Config(65536, 64, 16, 8, 3, 3, reweight_mode=1)),
+    ("C3p-L2", Config(65536, 64, 16, 8, 2, 2)),
+    ("C5-K4", Config(262144, 64, 16, 4, 3, 3)),
+    ("C5-K8", Config(262144, 64, 16, 8, 3, 3)),
+    ("C5-K16", Config(262144, 64, 16, 16, 3, 3)),
+    ("C5-K4-Le0", Config(262144, 64, 16, 4, 3, 0)),
+    ("C5-K8-Le0", Config(262144, 64, 16, 8, 3, 0)),
+    ("C5-K16-Le0", Config(262144, 64, 16, 16, 3, 0)),
+]
+TOL_MAX, TOL_FRO, TOL_ROW, TOL_LSE = 2e-2, 1e-2, 5e-2, 5e-3
+
+
+def _log_parity(rec: dict) -> None:
+    import json
+    import os
+    path = os.environ.get("LLSA_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+@pytest.mark.parametrize("name,cfg", REF_CASES, ids=[c[0] for c in REF_CASES])
+def test_full_size_tensor_core_path_matches_reference(reference, name, cfg):
+    import os
+    import time
+    reference.set_threads(os.cpu_count() or 1)
+    q, k, v, dO = unit_inputs(cfg, 0, bf16=True, backend=reference)
+    t0 = time.perf_counter()
+    ref = reference.run(cfg, q, k, v, dO)
+    ref_s = time.perf_counter() - t0
     lc = llsa.LLSAConfig(cfg.n, 64, 16, cfg.top_k, cfg.levels, cfg.enrich_levels,
                          reweight_mode=cfg.reweight_mode)
     h = llsa.LLSAHandle(lc, 1, torch.bfloat16)
     assert h.uses_tensor_cores
-    out = h.forward(q, k, v)
-    dq, dk, dv = h.backward(dO, q, k, v, out)
+    tq, tk, tv, tdo = (T(a, torch.bfloat16)[None] for a in (q, k, v, dO))
+    out = h.forward(tq, tk, tv)
+    dq, dk, dv = h.backward(tdo, tq, tk, tv, out)
     llsa.sync_status()
-    vc = llsa.validate_config(lc)
-    pq, pk, pv = (llsa.build_pyramid(t, 16, cfg.levels) for t in (q, k, v))
-    tables = llsa.hierarchical_topk(pq, pk, vc)
-    assert torch.equal(h.view("tables").view(-1), tables.view(-1))
-    st = llsa.llsa_forward(q, k, v, pk, pv, tables, vc)
-    tr = llsa.transpose_all(tables, vc)
-    rq, rk, rv = llsa.llsa_backward(dO, st, q, k, v, pk, pv, tables, tr, vc)
-    llsa.sync_status()
-    for name, got, want in (("out", out, st.output), ("dq", dq, rq), ("dk", dk, rk),
-                            ("dv", dv, rv)):
-        e = rel_err(got[0].cpu().numpy(), want[0].cpu().numpy())
-        assert e["max_rel"] <= 2e-2, (name, e)
-
+    rec = {"case": name, "n": cfg.n, "top_k": cfg.top_k, "levels": cfg.levels,
+           "enrich_levels": cfg.enrich_levels,
+           "mode": "LogitBias" if cfg.reweight_mode else "ScaleKV",
+           "reference_s": round(ref_s, 3), "reference_threads": reference.threads()}
+    got_tables = U32(h.view("tables"))[0]
+    diff_rows = 0
+    for l, (gt, wt) in enumerate(zip(cfg.split_tables(got_tables),
+                                     cfg.split_tables(ref.tables))):
+        diff_rows += int((gt != wt).any(axis=1).sum())
+    rec["table_rows_differing"] = diff_rows
+    for nm, got, want in (("out", out, ref.out), ("dq", dq, ref.dq), ("dk", dk, ref.dk),
+                          ("dv", dv, ref.dv)):
+        rec[nm] = rel_err(got[0].cpu().numpy(), want)
+    g_lse = lse(h.view("row_max")[0].cpu().numpy(), h.view("row_denom")[0].cpu().numpy())
+    rec["lse_max_abs"] = float(np.abs(g_lse - lse(ref.row_max, ref.row_denom)).max())
+    _log_parity(rec)
+    assert diff_rows == 0, rec
+    np.testing.assert_array_equal(got_tables, ref.tables)
+    for nm in ("out", "dq", "dk", "dv"):
+        e = rec[nm]
+        assert e["max_rel"] <= TOL_MAX and e["fro"] <= TOL_FRO and e["worst_row"] <= TOL_ROW, \
+            (nm, rec)
+    assert rec["lse_max_abs"] <= TOL_LSE, rec
 
 
 # The persistent tcgen05 kernels walk (unit, tile) work items; a multi-unit
