@@ -486,7 +486,9 @@ def unit_inputs(cfg: Config, unit: int, seed: int = 42, bf16: bool = True,
 
 
 def rel_err(a, ref) -> dict:
-    """max|Δ|/max|ref|, relative Frobenius and worst-row relative error."""
+    """max|Δ|/max|ref|, relative Frobenius, and the worst and 99th-percentile
+    row-relative error over rows whose reference norm is at least 1e-3 of the
+    largest row norm."""
     a = np.asarray(a, np.float64)
     ref = np.asarray(ref, np.float64)
     diff = a - ref
@@ -495,11 +497,13 @@ def rel_err(a, ref) -> dict:
     if ref.ndim == 2:
         rn = np.linalg.norm(ref, axis=1)
         keep = rn > 1e-3 * max(float(rn.max()), 1e-30)   # ignore ~zero reference rows
-        worst_row = float((np.linalg.norm(diff, axis=1)[keep] / rn[keep]).max()) \
-            if keep.any() else 0.0
+        rr = np.linalg.norm(diff, axis=1)[keep] / rn[keep]
+        worst_row = float(rr.max()) if keep.any() else 0.0
+        p99_row = float(np.percentile(rr, 99)) if keep.any() else 0.0
     else:
-        worst_row = float(np.abs(diff).max() / mx)
-    return {"max_rel": float(np.abs(diff).max()) / mx, "fro": fro, "worst_row": worst_row}
+        worst_row = p99_row = float(np.abs(diff).max() / mx)
+    return {"max_rel": float(np.abs(diff).max()) / mx, "fro": fro, "worst_row": worst_row,
+            "p99_row": p99_row}
 
 
 def lse(row_max, row_denom):

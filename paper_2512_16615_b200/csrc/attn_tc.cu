@@ -190,7 +190,7 @@ __global__ void prep_kernel(const float* __restrict__ pk, const float* __restric
     khi[i] = ah;
     klo[i] = __float2bfloat16_rn(a - __bfloat162float(ah));
     vhi[i] = bh;
-    vlo[i] = __float2bfloat16_rn(b - __bfloat162float(bh));
+    vlo[i] = __float2bfloat16_rn(0.f);  // see tc.h: dP uses V'_hi, the forward's value
   }
 }
 
@@ -725,10 +725,7 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
     const uint64_t row0 = p.pyr_off[level] + blk * kBS;
     load_rows_async(sK, 0, p.khi + pyr_off + row0 * kD, kBS, lane, 32);
     load_rows_async(sK + 2 * kTile16, 0, p.vhi + pyr_off + row0 * kD, kBS, lane, 32);
-    if (use_lo) {
-      load_rows_async(sK + kTile16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
-      load_rows_async(sK + 3 * kTile16, 0, p.vlo + pyr_off + row0 * kD, kBS, lane, 32);
-    }
+    if (use_lo) load_rows_async(sK + kTile16, 0, p.klo + pyr_off + row0 * kD, kBS, lane, 32);
   } else {
     load_rows_async(sK, 0, p.k + in_off + blk * kBS * kD, kBS, lane, 32);
     load_rows_async(sK + 2 * kTile16, 0, p.v + in_off + blk * kBS * kD, kBS, lane, 32);
@@ -760,15 +757,12 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
   cp_async_wait<1>();
   __syncwarp();
 
-  uint32_t kf[4][4], kl[4][4], vf[4][4], vl[4][4];
+  uint32_t kf[4][4], kl[4][4], vf[4][4];
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     lda(sK, 0, ks, lane, kf[ks]);
     lda(sK + 2 * kTile16, 0, ks, lane, vf[ks]);
-    if (use_lo) {
-      lda(sK + kTile16, 0, ks, lane, kl[ks]);
-      lda(sK + 3 * kTile16, 0, ks, lane, vl[ks]);
-    }
+    if (use_lo) lda(sK + kTile16, 0, ks, lane, kl[ks]);
   }
   float dk[8][4], dv[8][4];
 #pragma unroll
@@ -811,10 +805,6 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
         ldb(sg, h * 16, ks, lane, b);  // dO rows as B
         mma16816(g[2 * h], vf[ks], b[0], b[1]);
         mma16816(g[2 * h + 1], vf[ks], b[2], b[3]);
-        if (use_lo) {
-          mma16816(g[2 * h], vl[ks], b[0], b[1]);
-          mma16816(g[2 * h + 1], vl[ks], b[2], b[3]);
-        }
       }
     }
     // P^T, dS^T: element (key row, query col = nt*8 + cc + e%2)
@@ -2450,10 +2440,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           const uint64_t o = (uint64_t)__shfl_sync(0xffffffffu, myrow, ch * 4 + e) * kD;
           load_block16_async(dst + e * 2048, p.khi + o, bl, lane);
           load_block16_async(dst + 16384 + e * 2048, p.vhi + o, bl, lane);
-          if (lo) {
-            load_block16_async(dst + 8192 + e * 2048, p.klo + o, bl, lane);
-            load_block16_async(dst + 24576 + e * 2048, p.vlo + o, bl, lane);
-          }
+          if (lo) load_block16_async(dst + 8192 + e * 2048, p.klo + o, bl, lane);
         }
         cp_async_mbar_arrive(bar(KFULL + s));
       }
@@ -2483,10 +2470,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             const uint64_t ag = desc_kmajor(sg + ks * kKStepKMajor);
             mma_bf16(tS, aq, desc_kmajor(st + ks * kKStepKMajor), idesc, ks > 0);
             mma_bf16(tP, ag, desc_kmajor(st + 16384 + ks * kKStepKMajor), idesc, ks > 0);
-            if (lo) {
-              mma_bf16(tS, aq, desc_kmajor(st + 8192 + ks * kKStepKMajor), idesc, 1);
-              mma_bf16(tP, ag, desc_kmajor(st + 24576 + ks * kKStepKMajor), idesc, 1);
-            }
+            if (lo) mma_bf16(tS, aq, desc_kmajor(st + 8192 + ks * kKStepKMajor), idesc, 1);
           }
           commit(bar(SREADY + b));
           trace_ev(p, 3, c, 0);
@@ -3189,7 +3173,7 @@ constexpr int kQRing = 4;
 template <bool LO>
 struct L {
   static constexpr int kKeyBufs = LO ? 1 : 2;
-  static constexpr int kKeyBuf = (LO ? 4 : 2) * kArr;  // Khi, Vhi (, Klo, Vlo)
+  static constexpr int kKeyBuf = (LO ? 3 : 2) * kArr;  // Khi, Vhi (, Klo)
   static constexpr int kOffQ = kKeyBufs * kKeyBuf;
   static constexpr int kOffP = kOffQ + kQRing * kQStage;  // P^T, dS^T x 2
   static constexpr int kOffBar = kOffP + 2 * 2 * 16384;
@@ -3311,10 +3295,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint64_t o = (base + (uint64_t)__shfl_sync(0xffffffffu, ids, b) * kBS) * kD;
         load_block16_async(dst + b * 2048, p.khi + o, bl, lane);
         load_block16_async(dst + kArr + b * 2048, p.vhi + o, bl, lane);
-        if (LO) {
-          load_block16_async(dst + 2 * kArr + b * 2048, p.klo + o, bl, lane);
-          load_block16_async(dst + 3 * kArr + b * 2048, p.vlo + o, bl, lane);
-        }
+        if (LO) load_block16_async(dst + 2 * kArr + b * 2048, p.klo + o, bl, lane);
       }
       cp_async_mbar_arrive(bar(KFULL + kb));
     }
@@ -3341,10 +3322,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
             const uint64_t bg = desc_kmajor(sG + ks * kKStepKMajor);
             mma_bf16(tS, desc_kmajor(sK + ks * kKStepKMajor), bq, idesc_s, ks > 0);
             mma_bf16(tP, desc_kmajor(sK + kArr + ks * kKStepKMajor), bg, idesc_s, ks > 0);
-            if (LO) {
-              mma_bf16(tS, desc_kmajor(sK + 2 * kArr + ks * kKStepKMajor), bq, idesc_s, 1);
-              mma_bf16(tP, desc_kmajor(sK + 3 * kArr + ks * kKStepKMajor), bg, idesc_s, 1);
-            }
+            if (LO) mma_bf16(tS, desc_kmajor(sK + 2 * kArr + ks * kKStepKMajor), bq, idesc_s, 1);
           }
           commit(bar(SREADY + b));
         }
@@ -3616,8 +3594,8 @@ TcParams make_params(const Geometry& g) {
   P.dbg = dg ? (uint32_t)atoi(dg) : 0u;
   const char* tr = getenv("LLSA_TRACE");
   P.trace = tr && tr[0] == '1' ? 1u : 0u;
-  const char* hl = getenv("LLSA_HILO_LEVEL");  // 1: hi + lo on every coarse level
-  P.hilo_level = hl ? (uint32_t)atoi(hl) : 2u;
+  const char* hl = getenv("LLSA_HILO_LEVEL");  // default: hi + lo on every coarse level
+  P.hilo_level = hl ? (uint32_t)atoi(hl) : 1u;
   coarse_slots(g, P);
   rows_layout(g, P);
   return P;

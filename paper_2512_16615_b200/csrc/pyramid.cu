@@ -7,6 +7,8 @@
 // input rows with 16-byte loads; a warp covers whole 128 B row segments, so
 // every HBM sector fetched is used.  HBM-bound: bytes = rows_in·d·sizeof(in)
 // + rows_out·d·4.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc.h"
@@ -179,6 +181,7 @@ struct PyrArgs {
   uint64_t n, pyr_rows, off[kMaxLevels + 2];
   float gain[kMaxLevels + 2];
   uint32_t units, L, bf16_in;
+  uint32_t zero_lo;  // bit t: tensor t's lo part is written as zeros (V': see tc.h)
 };
 
 __device__ __forceinline__ void emit(const PyrArgs& a, int t, uint64_t idx, float v0, float v1,
@@ -191,7 +194,8 @@ __device__ __forceinline__ void emit(const PyrArgs& a, int t, uint64_t idx, floa
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       h[i] = __float2bfloat16_rn(x[i]);
-      l[i] = __float2bfloat16_rn(x[i] - __bfloat162float(h[i]));
+      l[i] = (a.zero_lo >> t) & 1 ? __float2bfloat16_rn(0.f)
+                                  : __float2bfloat16_rn(x[i] - __bfloat162float(h[i]));
     }
     *reinterpret_cast<uint2*>(a.hi[t] + idx) =
         make_uint2(*reinterpret_cast<uint32_t*>(&h[0]) | 0u, *reinterpret_cast<uint32_t*>(&h[2]));
@@ -312,6 +316,7 @@ llsa_status fused_pyramids(const Geometry& g, uint32_t units, const void* q, con
   a.units = units;
   a.L = g.L;
   a.bf16_in = dt == LLSA_BF16 ? 1u : 0u;
+  a.zero_lo = 4u;  // V'_lo: the tensor cores multiply V'_hi only, forward and backward
   pyr12_kernel<<<dim3((unsigned)(units * (g.n / 512)), 3), 512, 0, s>>>(a);
   count_launch();
   LLSA_LAUNCH_CHECK("pyr12_kernel");

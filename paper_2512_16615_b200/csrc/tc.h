@@ -12,6 +12,14 @@ namespace llsa_impl {
 struct TcBuffers {
   // Coarse levels 1..L, pre-scaled by the level's key/value gain and split
   // into bf16 hi + lo parts (SURVEY.md hard part 3): [units][pyr_rows][64].
+  // K' uses both parts in every score (S forward and backward, so the
+  // backward's P = exp(S - lse) matches the forward's).  V' is multiplied
+  // by its hi part only, in P·V AND in dP = dO·V'^T: the backward is then
+  // the exact gradient of the forward that ran, and D = rowsum(dO∘O) equals
+  // Σ P·dP up to rounding.  (With dP on hi + lo, one-hot rows on a
+  // gain-4096 coarse key gave D - dP ≈ 2^-9·|dO||V'| instead of 0, and dq
+  // errors of ~200 where the reference has 0.)  v_lo is kept zero-filled
+  // for the mma.sync fallback kernels that still read it.
   __nv_bfloat16* k_hi = nullptr;
   __nv_bfloat16* k_lo = nullptr;
   __nv_bfloat16* v_hi = nullptr;
