@@ -31,6 +31,25 @@ N_TOK, D, B, K, LEVELS = 65536, 64, 16, 8, 3
 UNITS_PER_GPU = 16
 METRIC = "LLSA fwd+bwd ms at N=65536 (256² px tokens) and % of tensor/HBM roofline"
 
+# BASELINE.json configs as bench presets (SURVEY.md §8 resolves "levels": the
+# reference's `levels` L = max_levels(N, 16); C5's "5 levels" is inadmissible
+# at N = 262144, so L = 3 = max).  C1 (N = 4096, fp32, 1 head) is the CPU
+# reference's own case and a parity test, not a bench line.
+PRESETS = {
+    "C2": dict(n=16384, levels=2, top_k=8, enrich_levels=2, units=16, global_units=0,
+               baseline="configs[1]: N=16384, 3 levels, 16 heads, bf16 fwd+bwd"),
+    "C3": dict(n=65536, levels=3, top_k=8, enrich_levels=3, units=16, global_units=0,
+               baseline="configs[2]: N=65536, 4 levels, 16 heads (headline metric)"),
+    "C4": dict(n=65536, levels=3, top_k=8, enrich_levels=3, units=16, global_units=128,
+               baseline="configs[3]: N=65536 fwd+bwd, batch 8 x 16 heads over 1/2/4/8 GPUs"),
+}
+for _k in (4, 8, 16):
+    for _le in (3, 0):
+        PRESETS[f"C5-K{_k}-Le{_le}"] = dict(
+            n=262144, levels=3, top_k=_k, enrich_levels=_le, units=16, global_units=0,
+            baseline=f"configs[4]: N=262144, K={_k}, "
+                     f"{'full' if _le == 3 else 'no'} KV enrichment")
+
 
 def _peaks() -> tuple[dict, str]:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -41,49 +60,88 @@ def _peaks() -> tuple[dict, str]:
         "fallback"
 
 
-def _geometry(n: int, L: int, k: int = K, b: int = B, d: int = D):
-    E = k * L + n // b ** (L + 1)
-    pairs = n * E * b                  # (query, key) pairs per unit, P = N·E·B
-    fine_pairs = n * k * b             # level-0 part
-    return E, pairs, fine_pairs
+def _geometry(n: int, L: int, k: int = K, b: int = B, le: int | None = None):
+    le = L if le is None else le
+    lim = min(le + 1, L)
+    top = n // b ** (L + 1) if le == L else 0      # coarsest blocks every query sees
+    E = k * lim + top
+    return {"E": E, "P": n * E * b,                # (query, key) pairs per unit, P = N·E·B
+            "P_fine": n * k * b,                   # level 0
+            "P_coarse": n * k * b * (lim - 1),     # levels 1 .. lim-1 (selected)
+            "P_top": n * top * b}                  # coarsest level (all N queries)
 
 
-def algorithmic_work(n: int, L: int, units: int) -> dict:
-    """Per-stage algorithmic work for `units` units."""
-    E, P, Pf = _geometry(n, L)
-    d = D
+def algorithmic_work(n: int, L: int, units: int, le: int | None = None, k: int = K) -> dict:
+    """Algorithmic work per timed stage for `units` units: SURVEY.md §8(d)'s
+    per-unit figures, split per kernel as DESIGN.md §3 states them.  bytes are
+    the minimum HBM traffic with bf16 tensors in and out (§8(d)); bytes_f32out
+    the same with the fp32 outputs this build writes (O, dq, dk, dv)."""
+    g = _geometry(n, L, k, le=le)
+    d, Nd, N = D, n * D, n
     pyr_rows = sum(n // B ** l for l in range(1, L + 1))
-    sel_macs = (n // B ** L) ** 2 * d + sum((n // B ** l) * K * B * d for l in range(1, L))
-    return {
-        # bytes: read q,k,v bf16, write fp32 pyramids of the three
-        "compress": {"bytes": units * (3 * n * d * 2 + 3 * pyr_rows * d * 4), "flops": 0},
-        "select": {"bytes": units * (2 * pyr_rows * d * 4), "flops": units * 2 * sel_macs},
-        # forward: QK^T + PV = 4·d·P; bytes: q,k,v bf16 in, O fp32 + (m, l) out
-        "fwd_attention": {"flops": units * 4 * d * P,
-                          "bytes": units * (3 * n * d * 2 + n * d * 4 + 2 * n * 4)},
-        "transpose": {"bytes": units * 3 * 4 * sum((n // B ** (l + 1)) * K for l in range(L)),
-                      "flops": 0},
-        # backward: 10·d·P (S, dP, dV, dQ, dK); bytes: q,k,v,dO bf16 + O fp32 + stats in,
-        # dq,dk,dv fp32 out
-        "backward": {"flops": units * 10 * d * P,
-                     "bytes": units * (4 * n * d * 2 + n * d * 4 + 2 * n * 4 + 3 * n * d * 4)},
-        "pairs": units * P, "fine_pairs": units * Pf, "E": E,
+    sel_macs = (n // B ** L) ** 2 * d + sum((n // B ** l) * k * B * d for l in range(1, L))
+    tr_entries = sum((n // B ** (l + 1)) * k for l in range(L))
+    w = {
+        # read q, k, v (bf16); write the fp32 pooled levels of the three
+        "compress": {"flops": 0, "bytes": 3 * Nd * 2 + 3 * pyr_rows * d * 4},
+        # exact fp32 scores (2 flops per MAC) over the pooled q, k
+        "select": {"flops": 2 * sel_macs, "bytes": 2 * pyr_rows * d * 4 + tr_entries * 4},
+        # QK^T + PV = 4·d·P; read Q, K, V, write O + LSE (8·N·d + 4·N; + row_max and
+        # row_denom = 8·N·d + 8·N as stored)
+        "fwd_attention": {"flops": 4 * d * g["P"], "bytes": 8 * Nd + 8 * N,
+                          "bytes_f32out": 6 * Nd + 4 * Nd + 8 * N},
+        # CSR → CSC: read the tables, write offsets + lists (int32)
+        "transpose": {"flops": 0, "bytes": 3 * 4 * tr_entries},
+        # S, dP, dQ over every pair (6·d·P); read Q, K, V, O, dO, LSE; write dq, D
+        "bwd_dq": {"flops": 6 * d * g["P"], "bytes": 12 * Nd + 8 * N,
+                   "bytes_f32out": 8 * Nd + 4 * Nd + 4 * Nd + 8 * N},
+        # S, dP, dK', dV' over the selected coarse pairs (levels 1..L_e); read Q, dO,
+        # LSE, D once; the pooled K', V' rows and gradients are small
+        "bwd_kv_coarse_tc5": {"flops": 8 * d * g["P_coarse"],
+                              "bytes": 4 * Nd + 8 * N + 4 * pyr_rows * d * 2},
+        # coarsest level against all N queries: read Q, dO, LSE, D
+        "bwd_kv_coarse": {"flops": 8 * d * g["P_top"], "bytes": 4 * Nd + 8 * N},
+        # S, dP, dK, dV over the fine pairs (8·d·P_fine); read Q, K, V, dO, LSE, D,
+        # write dK, dV (12·N·d + 8·N; fp32 dK, dV: 16·N·d + 8·N)
+        "bwd_kv_fine": {"flops": 8 * d * g["P_fine"], "bytes": 12 * Nd + 8 * N,
+                        "bytes_f32out": 8 * Nd + 8 * Nd + 8 * N},
     }
+    for v in w.values():
+        v["flops"] *= units
+        v["bytes"] *= units
+        if "bytes_f32out" in v:
+            v["bytes_f32out"] *= units
+    # whole-path totals (§8(d)): forward 4·d·P, backward 10·d·P FLOP;
+    # forward 8·N·d + 4·N, backward 16·N·d + 8·N bytes
+    w["fwd_total"] = {"flops": units * 4 * d * g["P"], "bytes": units * (8 * Nd + 4 * N)}
+    w["bwd_total"] = {"flops": units * 10 * d * g["P"], "bytes": units * (16 * Nd + 8 * N)}
+    w["pairs"], w["E"] = units * g["P"], g["E"]
+    return w
 
 
-def stage_work(name: str, W: dict) -> dict:
-    """Algorithmic work attributed to one timed stage of the handle."""
-    if name in W and isinstance(W[name], dict):
-        return W[name]
-    bw = W["backward"]
-    P, Pf = W["pairs"], W["fine_pairs"]
-    if name in ("bwd_dq", "bwd_dq_tc"):          # S, dP, dQ over all pairs
-        return {"flops": bw["flops"] * 6 // 10, "bytes": bw["bytes"] // 2}
-    if name.startswith("bwd_kv_fine"):           # dK, dV over fine pairs
-        return {"flops": bw["flops"] * 4 // 10 * Pf // P, "bytes": bw["bytes"] // 3}
-    if name.startswith("bwd_kv"):                # dK, dV over coarse pairs
-        return {"flops": bw["flops"] * 4 // 10 * (P - Pf) // P, "bytes": bw["bytes"] // 6}
-    return {"flops": 0, "bytes": 0}
+def stage_roofline(name: str, ms: float, W: dict, peaks: dict) -> dict | None:
+    """Tensor and HBM fractions of one stage; `bound` is the roof its
+    algorithmic work hits first (max of the two ideal times)."""
+    wk = W.get(name)
+    if not wk or ms <= 0:
+        return None
+    pt, ph = peaks["bf16_tflops"], peaks["hbm_gbs"]
+    tflops = wk["flops"] / (ms * 1e-3) / 1e12
+    gbs = wk["bytes"] / (ms * 1e-3) / 1e9
+    t_tc = wk["flops"] / (pt * 1e12)
+    t_hbm = wk["bytes"] / (ph * 1e9)
+    r = {"ms": round(ms, 4), "flops": wk["flops"], "bytes": wk["bytes"],
+         "tflops": round(tflops, 2), "tensor_frac": round(tflops / pt, 4),
+         "gbs": round(gbs, 1), "hbm_frac": round(gbs / ph, 4),
+         "bound": "tensor" if t_tc >= t_hbm else "hbm",
+         "ideal_ms": round(max(t_tc, t_hbm) * 1e3, 4)}
+    if "bytes_f32out" in wk:
+        r["hbm_frac_f32out"] = round(wk["bytes_f32out"] / (ms * 1e-3) / 1e9 / ph, 4)
+    tr = _traffic(name)
+    if tr:
+        r["traffic"] = tr
+        r["traffic_over_algorithmic"] = round(tr / wk["bytes"], 3)
+    return r
 
 
 class ClockSampler:
@@ -155,34 +213,47 @@ class ClockSampler:
 # reference CPU arm
 # ---------------------------------------------------------------------------
 def reference_sample(steps: int, warmup: int, n: int = N_TOK, L: int = LEVELS,
-                     units: int = UNITS_PER_GPU) -> dict:
-    """Times the reference library (oracle/_ref, all host threads) on one unit
-    of the workload per step; reports ms for the full `units`-unit step."""
-    import numpy as np
+                     units: int = UNITS_PER_GPU, k: int = K, le: int | None = None) -> dict:
+    """Times the reference library (oracle/_ref: the unmodified reference
+    compiled from its sources, f32 build) on the WHOLE step: all `units`
+    units, each through the reference's full path (compress, select, plan,
+    forward, transpose, backward), the units run concurrently on host threads
+    (the library is reentrant; its own parallel_for uses every core inside
+    each call), so a step is the same work as the GPU arm's step."""
+    from concurrent.futures import ThreadPoolExecutor
 
     from oracle import REF_SO, Config, OracleC, Reference, unit_inputs
-    cfg = Config(n, D, B, K, L, L)
+    cfg = Config(n, D, B, k, L, L if le is None else le)
     if os.path.exists(REF_SO[32]):
         be = Reference(32)
         be.set_threads(0)
         kind, cores = "reference", be.threads()
-    else:  # reference not compiled on this box: the C restatement (1 thread)
+        kw = {"want_outputs": False}
+    else:  # reference not compiled on this box: the C restatement (1 thread per unit)
         be = OracleC()
-        kind, cores = "port", 1
-    q, k, v, dO = unit_inputs(cfg, 0, backend=be)
+        kind, cores = "port", os.cpu_count() or 1
+        kw = {}
+    ins = [unit_inputs(cfg, u, backend=be) for u in range(units)]
+    pool = ThreadPoolExecutor(max_workers=units)
+
+    def one_step():
+        list(pool.map(lambda x: be.run(cfg, *x, **kw), ins))
+
     times = []
     for i in range(warmup + steps):
         t0 = time.perf_counter()
-        be.run(cfg, q, k, v, dO, **({"want_outputs": False} if kind == "reference" else {}))
+        one_step()
         dt = (time.perf_counter() - t0) * 1e3
         if i >= warmup:
             times.append(dt)
-    per_unit = statistics.median(times)
-    return {"value": per_unit * units, "unit": "ms", "cores": cores, "kind": kind,
-            "sample": f"1 of {units} units per step (N={n}, L={L}, fwd+bwd incl. "
-                      f"compress/select/plan/transpose), median of {steps} after {warmup} "
-                      f"warm-up, x{units} units; {os.cpu_count()} host CPUs",
-            "per_unit_ms": per_unit}
+    pool.shutdown()
+    per_step = statistics.fmean(times)   # total / steps, like the GPU arm
+    return {"value": per_step, "unit": "ms", "cores": cores, "kind": kind,
+            "sample": f"all {units} units per step (N={n}, L={L}, K={k}, fwd+bwd incl. "
+                      f"compress/select/plan/transpose), units concurrent on host threads, "
+                      f"mean of {steps} step(s) after {warmup} warm-up; "
+                      f"{os.cpu_count()} host CPUs",
+            "steps": steps, "warmup": warmup, "median_ms": statistics.median(times)}
 
 
 # ---------------------------------------------------------------------------
@@ -249,11 +320,16 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="llsa", choices=["llsa", "reference"])
-    ap.add_argument("--n", type=int, default=N_TOK)
-    ap.add_argument("--levels", type=int, default=LEVELS)
-    ap.add_argument("--units", type=int, default=UNITS_PER_GPU,
+    ap.add_argument("--config", default="C3", choices=sorted(PRESETS),
+                    help="BASELINE.json workload preset (SURVEY.md §8 C2..C5); C3 is the "
+                         "headline metric's config")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--levels", type=int, default=None)
+    ap.add_argument("--top-k", type=int, default=None)
+    ap.add_argument("--enrich-levels", type=int, default=None)
+    ap.add_argument("--units", type=int, default=None,
                     help="units per GPU (weak scaling, default)")
-    ap.add_argument("--global-units", type=int, default=0,
+    ap.add_argument("--global-units", type=int, default=None,
                     help="fixed total units split over the GPUs (strong scaling, e.g. 128 "
                          "for BASELINE C4 = batch 8 x 16 heads)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -264,6 +340,10 @@ def main() -> None:
                     help="skip the dense SDPA comparator")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    preset = PRESETS[args.config]
+    for key in ("n", "levels", "top_k", "enrich_levels", "units", "global_units"):
+        if getattr(args, key) is None:
+            setattr(args, key, preset[key])
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -273,11 +353,14 @@ def main() -> None:
     if args.global_units:
         args.units = shard_units(args.global_units, world, rank)[1]
         scaling = "strong"
-    cfg_json = {"workload": f"LLSA fwd+bwd, N={args.n}, {args.units} units (batch·head) per "
-                            f"GPU, d=64, B=16, K=8, L={args.levels} (BASELINE '4 levels'), "
-                            "L_e=L, ScaleKV, bf16 in / fp32 out",
-                "n": args.n, "d": D, "block_size": B, "top_k": K, "levels": args.levels,
-                "enrich_levels": args.levels, "units_per_gpu": args.units,
+    cfg_json = {"workload": f"LLSA fwd+bwd ({args.config}), N={args.n}, {args.units} units "
+                            f"(batch·head) per GPU, d=64, B=16, K={args.top_k}, "
+                            f"L={args.levels}, L_e={args.enrich_levels}, ScaleKV, bf16 in / "
+                            "fp32 out",
+                "preset": args.config, "baseline_config": preset["baseline"],
+                "n": args.n, "d": D, "block_size": B, "top_k": args.top_k,
+                "levels": args.levels, "enrich_levels": args.enrich_levels,
+                "units_per_gpu": args.units,
                 "global_units": args.global_units or args.units * world,
                 "parallelism": f"batch*head units sharded over {world} GPU(s), no collective",
                 "l2": "inputs larger than L2 (4 x units x N x 64 bf16 per step)"}
@@ -285,9 +368,12 @@ def main() -> None:
     if args.impl == "reference":
         if rank != 0:
             return
-        r = reference_sample(args.steps, args.warmup, args.n, args.levels, args.units)
+        # a CPU library has nothing to warm beyond page faults: one warm-up step
+        r = reference_sample(args.steps, 1, args.n, args.levels, args.units, args.top_k,
+                             args.enrich_levels)
         line = {"metric": METRIC, "value": r["value"], "unit": "ms", "impl": "reference",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": 1,
+                "warmup_requested": args.warmup,
                 "ms_per_step": r["value"], "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_random "
                 "N(0,1), bf16-rounded)", "config": cfg_json,
@@ -319,7 +405,7 @@ def main() -> None:
     shape = (units, n, D)
     q, k, v, dO = (torch.randn(shape, generator=gen, device=dev).to(torch.bfloat16)
                    for _ in range(4))
-    cfg = llsa.LLSAConfig(n, D, B, K, args.levels, args.levels)
+    cfg = llsa.LLSAConfig(n, D, B, args.top_k, args.levels, args.enrich_levels)
     h = llsa.LLSAHandle(cfg, units, torch.bfloat16)
     h.enable_timing(True)
     out = torch.empty(shape, device=dev, dtype=torch.float32)
@@ -379,30 +465,31 @@ def main() -> None:
     from paper_2512_16615_b200.sharding import max_over_ranks
     ms = max_over_ranks(ms)
 
-    # ---- roofline of the dominant kernel (stage) ----------------------------
+    # ---- roofline: every stage, and the dominant one as the headline --------
     peaks, peak_src = _peaks()
-    W = algorithmic_work(n, args.levels, units)
-    dom_name, dom_ms = max(stages, key=lambda s: s[1]) if stages else ("?", 0.0)
-    wk = stage_work(dom_name, W)
-    t_tc = wk["flops"] / (peaks["bf16_tflops"] * 1e12) if wk["flops"] else 0.0
-    t_hbm = wk["bytes"] / (peaks["hbm_gbs"] * 1e9) if wk["bytes"] else 0.0
-    if t_tc >= t_hbm:
-        achieved = wk["flops"] / (dom_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s"}
+    W = algorithmic_work(n, args.levels, units, args.enrich_levels, args.top_k)
+    per_stage = {s_: stage_roofline(s_, t_, W, peaks) for s_, t_ in stages}
+    per_stage = {k_: v_ for k_, v_ in per_stage.items() if v_}
+    dom_name = max(per_stage, key=lambda s_: per_stage[s_]["ms"]) if per_stage else "?"
+    dr = per_stage.get(dom_name, {})
+    if dr.get("bound") == "tensor":
+        roof = {"bound": "tensor", "achieved": dr["tflops"], "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": dr["tensor_frac"]}
     else:
-        achieved = wk["bytes"] / (dom_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _traffic(dom_name)
-    roof["kernel"] = dom_name
-    roof["kernel_ms"] = dom_ms
-    roof["peak_source"] = f"{peak_src} (MEASURED_PEAKS.json, burst)"
-    total_flops = W["fwd_attention"]["flops"] + W["backward"]["flops"]
-    ideal_ms = (max(W["fwd_attention"]["flops"] / (peaks["bf16_tflops"] * 1e12),
-                    W["fwd_attention"]["bytes"] / (peaks["hbm_gbs"] * 1e9)) +
-                max(W["backward"]["flops"] / (peaks["bf16_tflops"] * 1e12),
-                    W["backward"]["bytes"] / (peaks["hbm_gbs"] * 1e9))) * 1e3
+        roof = {"bound": "hbm", "achieved": dr.get("gbs"), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": dr.get("hbm_frac")}
+    roof["traffic"] = dr.get("traffic")
+    roof.update({"kernel": dom_name, "kernel_ms": dr.get("ms"),
+                 "algorithmic_bytes": dr.get("bytes"), "algorithmic_flops": dr.get("flops"),
+                 "tensor_frac": dr.get("tensor_frac"), "hbm_frac": dr.get("hbm_frac"),
+                 "traffic_over_algorithmic": dr.get("traffic_over_algorithmic"),
+                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json, burst)",
+                 "work_model": "SURVEY.md §8(d) per-unit bytes / FLOPs x units, per kernel "
+                               "as DESIGN.md §3; bench.algorithmic_work"})
+    total_flops = W["fwd_total"]["flops"] + W["bwd_total"]["flops"]
+    ideal_ms = sum(max(W[k_]["flops"] / (peaks["bf16_tflops"] * 1e12),
+                       W[k_]["bytes"] / (peaks["hbm_gbs"] * 1e9))
+                   for k_ in ("fwd_total", "bwd_total")) * 1e3
 
     # ---- end to end through the C ABI with host buffers -----------------------
     # Every step copies its inputs H2D from pinned host memory and its results
@@ -476,7 +563,7 @@ def main() -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = reference_sample(1, 1, n, args.levels, units)
+            r = reference_sample(1, 0, n, args.levels, units, args.top_k, args.enrich_levels)
             cpu = {k_: r[k_] for k_ in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "unavailable",
@@ -505,6 +592,7 @@ def main() -> None:
                 "ideal_ms": ideal_ms,
                 "roofline": roof,
                 "stages_ms": {s: round(t_, 4) for s, t_ in stages},
+                "stages_roofline": per_stage,
                 "eager_ms_per_step": eager_ms,
                 "timed_launch_mode": "cuda_graph_replay" if graph is not None else "eager",
                 "tensor_cores": h.uses_tensor_cores,
