@@ -8,7 +8,7 @@ for tool in memcheck racecheck synccheck; do
   for cfg in "16384 2" "65536 3"; do
     set -- $cfg
     log=gpurun_out/sanitize_${tool}_n$1.log
-    timeout 900 compute-sanitizer --tool $tool --kernel-name-exclude regex:at:: \
+    timeout 900 compute-sanitizer --tool $tool \
       python tools/memcheck_c3.py $1 $2 1 > $log 2>&1
     echo "$tool n=$1 rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' $log | tail -2 | tr '\n' ' ')"
   done
