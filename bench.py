@@ -313,6 +313,111 @@ def _traffic(stage: str):
         return None
 
 
+def run_e2e(kind: str, h, inputs, cfg, dev, stream, steps: int, barrier, max_over_ranks
+            ) -> dict:
+    """End to end through the C ABI with HOST buffers: every step copies its
+    inputs (q, k, v, dO bf16) H2D from pinned memory, runs the whole path and
+    copies its results (O, dq, dk, dv) D2H.  Steps are software-pipelined over
+    three streams with double-buffered device sets, so H2D of step i+1 and D2H
+    of step i-1 overlap step i's kernels (PCIe is full duplex) and the steady
+    state is bound by the larger transfer.
+      handle_bf16_out  llsa_handle_forward_ex / backward_ex, bf16 results
+      handle_f32_out   llsa_handle_forward / backward, fp32 results
+      staged_c_abi     the reference-shaped staged entry points (llsa_build_pyramid
+                       x3, llsa_hierarchical_topk, llsa_forward, llsa_transpose_all,
+                       llsa_backward; bf16 inputs run the same tensor-core kernels),
+                       fp32 results as the reference's ForwardState / GradientSet"""
+    import torch
+
+    import paper_2512_16615_b200 as llsa
+    q, k, v, dO = inputs
+    shape = q.shape
+    odt = torch.bfloat16 if kind == "handle_bf16_out" else torch.float32
+    hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, dO))
+    hout = [tuple(torch.empty(shape, dtype=odt).pin_memory() for _ in range(4))
+            for _ in range(2)]
+    din = [tuple(t.clone() for t in (q, k, v, dO)) for _ in range(2)]
+    dres = [tuple(torch.empty(shape, device=dev, dtype=odt) for _ in range(4))
+            for _ in range(2)]
+    vc = llsa.validate_config(cfg)
+    s_h2d, s_cmp, s_d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    in_free = [ev(), ev()]     # compute of the step that last used din[b] is done
+    res_free = [ev(), ev()]    # D2H of the step that last used dres[b] is done
+    for e_ in in_free + res_free:
+        e_.record(stream)
+
+    def compute(q_, k_, v_, g_, o_, dq_, dk_, dv_):
+        if kind != "staged_c_abi":
+            h.forward(q_, k_, v_, o_)
+            h.backward(g_, q_, k_, v_, o_, dq_, dk_, dv_)
+            return
+        L = vc.levels
+        pq, pk, pv = (llsa.build_pyramid(t, vc.block_size, L) for t in (q_, k_, v_))
+        tables = llsa.hierarchical_topk(pq, pk, vc)
+        st = llsa.llsa_forward(q_, k_, v_, pk, pv, tables, vc, check_finite=False)
+        tr = llsa.transpose_all(tables, vc)
+        gq, gk, gv = llsa.llsa_backward(g_, st, q_, k_, v_, pk, pv, tables, tr, vc)
+        for d_, s_ in zip((o_, dq_, dk_, dv_), (st.output, gq, gk, gv)):
+            d_.copy_(s_)
+
+    def e2e_steps(n_steps):
+        for i in range(n_steps):
+            b = i & 1
+            h2d_done, cmp_done = ev(), ev()
+            with torch.cuda.stream(s_h2d):
+                s_h2d.wait_event(in_free[b])
+                for d_, h_ in zip(din[b], (hq, hk, hv, hdo)):
+                    d_.copy_(h_, non_blocking=True)
+                h2d_done.record(s_h2d)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(h2d_done)
+                s_cmp.wait_event(res_free[b])
+                compute(*din[b], *dres[b])
+                cmp_done.record(s_cmp)
+                in_free[b] = ev()
+                in_free[b].record(s_cmp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(cmp_done)
+                for h_, d_ in zip(hout[b], dres[b]):
+                    h_.copy_(d_, non_blocking=True)
+                res_free[b] = ev()
+                res_free[b].record(s_d2h)
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps(2)
+    torch.cuda.synchronize()
+    llsa.sync_status()
+    n_e2e = max(3, min(steps, 10))
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for s_ in (s_h2d, s_cmp, s_d2h):
+        s_.wait_event(e0)
+    e2e_steps(n_e2e)
+    for s_ in (s_h2d, s_cmp, s_d2h):
+        stream.wait_stream(s_)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    llsa.sync_status()
+    ms = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
+    esz = 2 if odt == torch.bfloat16 else 4
+    res = {"value": ms, "unit": "ms", "h2d_bytes_per_step": 4 * q.numel() * 2,
+           "d2h_bytes_per_step": 4 * q.numel() * esz, "steps": n_e2e,
+           "outputs": str(odt).replace("torch.", ""),
+           "path": {"handle_bf16_out": "llsa_handle_forward_ex/backward_ex (C ABI), bf16 O/dq/"
+                                       "dk/dv",
+                    "handle_f32_out": "llsa_handle_forward/backward (C ABI), fp32 O/dq/dk/dv",
+                    "staged_c_abi": "staged reference-shaped C ABI (llsa_build_pyramid, "
+                                    "llsa_hierarchical_topk, llsa_forward, llsa_transpose_all, "
+                                    "llsa_backward), fp32 O/dq/dk/dv"}[kind]
+           + "; pinned host buffers, H2D / kernels / D2H pipelined over three streams"}
+    del din, dres, hout
+    torch.cuda.empty_cache()
+    return res
+
+
 # ---------------------------------------------------------------------------
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -497,68 +602,12 @@ def main() -> None:
     # streams with double-buffered device sets: H2D of step i+1 and D2H of
     # step i-1 overlap step i's kernels (PCIe is full duplex), so the
     # steady state is bound by the larger transfer, not by their sum.
-    e2e = None
+    e2e, e2e_variants = None, {}
     if not args.no_e2e:
-        hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, dO))
-        hout = [tuple(torch.empty(shape, dtype=torch.float32).pin_memory() for _ in range(4))
-                for _ in range(2)]
-        din = [tuple(t.clone() for t in (q, k, v, dO)) for _ in range(2)]
-        dres = [(out,) + (dq, dk, dv),
-                tuple(torch.empty(shape, device=dev, dtype=torch.float32) for _ in range(4))]
-        s_h2d, s_cmp, s_d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
-        ev = lambda: torch.cuda.Event()  # noqa: E731
-        in_free = [ev(), ev()]     # compute of the step that last used din[b] is done
-        res_free = [ev(), ev()]    # D2H of the step that last used dres[b] is done
-        for e_ in in_free + res_free:
-            e_.record(stream)
-
-        def e2e_steps(n_steps):
-            for i in range(n_steps):
-                b = i & 1
-                h2d_done, cmp_done = ev(), ev()
-                with torch.cuda.stream(s_h2d):
-                    s_h2d.wait_event(in_free[b])
-                    for d_, h_ in zip(din[b], (hq, hk, hv, hdo)):
-                        d_.copy_(h_, non_blocking=True)
-                    h2d_done.record(s_h2d)
-                with torch.cuda.stream(s_cmp):
-                    s_cmp.wait_event(h2d_done)
-                    s_cmp.wait_event(res_free[b])
-                    q_, k_, v_, g_ = din[b]
-                    o_, dq_, dk_, dv_ = dres[b]
-                    h.forward(q_, k_, v_, o_)
-                    h.backward(g_, q_, k_, v_, o_, dq_, dk_, dv_)
-                    cmp_done.record(s_cmp)
-                    in_free[b] = ev()
-                    in_free[b].record(s_cmp)
-                with torch.cuda.stream(s_d2h):
-                    s_d2h.wait_event(cmp_done)
-                    for h_, d_ in zip(hout[b], dres[b]):
-                        h_.copy_(d_, non_blocking=True)
-                    res_free[b] = ev()
-                    res_free[b].record(s_d2h)
-
-        e2e_steps(2)
-        torch.cuda.synchronize()
-        n_e2e = max(3, min(args.steps, 10))
-        barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for s_ in (s_h2d, s_cmp, s_d2h):
-            s_.wait_event(e0)
-        e2e_steps(n_e2e)
-        for s_ in (s_h2d, s_cmp, s_d2h):
-            stream.wait_stream(s_)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms = e0.elapsed_time(e1) / n_e2e
-        e2e_ms = max_over_ranks(e2e_ms)
-        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 4 * q.numel() * 2,
-               "d2h_bytes_per_step": 4 * out.numel() * 4, "steps": n_e2e,
-               "path": "llsa_handle_forward/backward (C ABI) with pinned host buffers; "
-                       "H2D / kernels / D2H pipelined across steps on three streams"}
-        del din, dres, hout
+        e2e_variants = {k_: run_e2e(k_, h, (q, k, v, dO), cfg, dev, stream, args.steps,
+                                    barrier, max_over_ranks)
+                        for k_ in ("handle_bf16_out", "handle_f32_out", "staged_c_abi")}
+        e2e = dict(e2e_variants["handle_bf16_out"])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -596,7 +645,7 @@ def main() -> None:
                 "eager_ms_per_step": eager_ms,
                 "timed_launch_mode": "cuda_graph_replay" if graph is not None else "eager",
                 "tensor_cores": h.uses_tensor_cores,
-                "cpu_baseline": cpu, "e2e": e2e, "dense_sdpa": dense, "gpu_launches": launches * args.steps,
+                "cpu_baseline": cpu, "e2e": e2e, "e2e_variants": e2e_variants, "dense_sdpa": dense, "gpu_launches": launches * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -282,6 +282,19 @@ llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k,
 llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q,
                                  const void* k, const void* v, const float* out,
                                  float* dq, float* dk, float* dv, void* stream);
+/* The same two calls with the outputs in `out_dtype`: LLSA_F32 is exactly
+ * llsa_handle_forward / llsa_handle_backward; LLSA_BF16 writes out, dq, dk,
+ * dv as bf16 (RNE of the fp32 results; half the bytes to move off the GPU).
+ * In bf16 mode the handle keeps the fp32 output internally for the backward's
+ * D = rowsum(dO∘O), so `out` given to the backward must be the bf16 output of
+ * the handle's latest forward (else LLSA_ERR_STALE_STATE). */
+llsa_status llsa_handle_forward_ex(llsa_handle h, const void* q, const void* k,
+                                   const void* v, void* out, llsa_dtype out_dtype,
+                                   void* stream);
+llsa_status llsa_handle_backward_ex(llsa_handle h, const void* d_out, const void* q,
+                                    const void* k, const void* v, const void* out,
+                                    void* dq, void* dk, void* dv, llsa_dtype out_dtype,
+                                    void* stream);
 llsa_status llsa_handle_buffer(llsa_handle h, llsa_buffer which, void** ptr,
                                size_t* bytes);
 /* Number of kernel launches the last forward / backward issued. */

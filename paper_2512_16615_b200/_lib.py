@@ -105,6 +105,8 @@ SIGNATURES = {
     "llsa_handle_uses_tensor_cores": (C.c_int, [_vp]),
     "llsa_handle_forward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "llsa_handle_backward": (C.c_int, [_vp] + [_vp] * 8 + [_vp]),
+    "llsa_handle_forward_ex": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_int, _vp]),
+    "llsa_handle_backward_ex": (C.c_int, [_vp] + [_vp] * 8 + [C.c_int, _vp]),
     "llsa_handle_buffer": (C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_sz)]),
     "llsa_handle_last_launches": (_u32, [_vp]),
     "llsa_handle_enable_timing": (C.c_int, [_vp, C.c_int]),

@@ -26,11 +26,13 @@ class _LLSAFunction(torch.autograd.Function):
         units = q.shape[0] * q.shape[1]
         h = module._handle_for(units, q)
         x = [t.reshape(units, t.shape[-2], t.shape[-1]).contiguous() for t in (q, k, v)]
-        out = h.forward(*x)
+        # outputs in the input dtype straight from the handle (bf16 mode keeps
+        # the fp32 O the backward needs inside the handle)
+        out = h.forward(*x, out_dtype=q.dtype)
         module._generation += 1
         ctx.module, ctx.generation, ctx.shape = module, module._generation, q.shape
         ctx.save_for_backward(*x, out)
-        return out.view(q.shape).to(q.dtype)
+        return out.view(q.shape)
 
     @staticmethod
     def backward(ctx, grad):
@@ -41,8 +43,7 @@ class _LLSAFunction(torch.autograd.Function):
         g = grad.reshape(out.shape).to(q.dtype).contiguous()
         dq, dk, dv = m._handle.backward(g, q, k, v, out)
         shape = ctx.shape
-        return (dq.view(shape).to(q.dtype), dk.view(shape).to(k.dtype),
-                dv.view(shape).to(v.dtype), None)
+        return dq.view(shape), dk.view(shape), dv.view(shape), None
 
 
 class LLSAAttention(torch.nn.Module):

@@ -3700,6 +3700,11 @@ static llsa_status launch_prep(const Geometry& g, uint32_t units, const float* p
   return LLSA_OK;
 }
 
+llsa_status tc_prep(const Geometry& g, uint32_t units, const float* pyr_k, const float* pyr_v,
+                    const TcBuffers& tb, cudaStream_t s) {
+  return launch_prep(g, units, pyr_k, pyr_v, tb, s);
+}
+
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,

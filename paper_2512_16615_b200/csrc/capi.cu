@@ -466,6 +466,18 @@ llsa_status llsa_forward(const llsa_config* cfg, uint32_t units, llsa_dtype dt, 
   NONNULL(rm);
   NONNULL(rd);
   if (g.L >= 1 && (!pyr_k || !pyr_v)) return fail(LLSA_ERR_ARGUMENT, "null pyramid");
+  if (tc_supported(g, dt)) {
+    // the handle's tensor-core kernels; the K'/V' operand copies live in a
+    // stream-ordered allocation for the duration of the call
+    cudaStream_t s = S(stream);
+    void* buf = nullptr;
+    LLSA_CUDA_TRY(cudaMallocAsync(&buf, tc_buffer_bytes(g, units), s));
+    TcBuffers tb;
+    tc_carve(g, units, static_cast<char*>(buf), &tb);
+    llsa_status st = tc_forward(g, units, q, k, v, pyr_k, pyr_v, tables, out, rm, rd, tb, s);
+    cudaFreeAsync(buf, s);
+    return st;
+  }
   return simt_forward(g, units, dt, q, k, v, pyr_k, pyr_v, tables, out, rm, rd, S(stream));
 }
 
@@ -522,10 +534,33 @@ llsa_status llsa_backward_plan(const llsa_config* cfg, uint32_t units, llsa_dtyp
                        flat, dq, dk, dv, ws, S(stream), nullptr, &plan);
 }
 
+namespace {
+// Workspace of the staged tensor-core backward: K'/V' operand copies, the
+// kernels' own scratch, and (kv_backward only) rebuilt tables + a scratch dq.
+struct TcStagedWs {
+  size_t tcb, bwd, tab, cur, dq, total;
+  TcStagedWs(const Geometry& g, uint32_t units) {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    tcb = al(tc_buffer_bytes(g, units));
+    bwd = al(tc_backward_ws_bytes(g, units));
+    tab = al((size_t)units * g.table_entries * 4);
+    cur = al(tables_from_csc_ws(g, units));
+    dq = al((size_t)units * g.n * g.d * 4);
+    total = tcb + bwd + tab + cur + dq;
+  }
+};
+size_t backward_ws(const Geometry& g, uint32_t units) {
+  const size_t simt = simt_backward_ws_bytes(g, units);
+  if (!tc_supported(g, LLSA_BF16)) return simt;
+  const size_t tc = TcStagedWs(g, units).total;
+  return tc > simt ? tc : simt;
+}
+}  // namespace
+
 size_t llsa_backward_workspace_bytes(const llsa_config* cfg, uint32_t units) {
   Geometry g;
   if (make_geometry(cfg, &g)) return 0;
-  return simt_backward_ws_bytes(g, units);
+  return backward_ws(g, units);
 }
 
 llsa_status llsa_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
@@ -553,8 +588,18 @@ llsa_status llsa_backward(const llsa_config* cfg, uint32_t units, llsa_dtype dt,
   NONNULL(dq);
   NONNULL(dk);
   NONNULL(dv);
-  if (!ws || ws_bytes < simt_backward_ws_bytes(g, units))
+  if (!ws || ws_bytes < backward_ws(g, units))
     return fail(LLSA_ERR_ARGUMENT, "backward workspace too small");
+  if (tc_supported(g, dt)) {
+    const TcStagedWs w(g, units);
+    char* p = static_cast<char*>(ws);
+    TcBuffers tb;
+    tc_carve(g, units, p, &tb);
+    cudaStream_t s = S(stream);
+    if (llsa_status st = tc_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
+    return tc_backward(g, units, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, tables, offs, flat,
+                       dq, dk, dv, tb, p + w.tcb, s);
+  }
   return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, tables, offs,
                        flat, dq, dk, dv, ws, S(stream));
 }
@@ -582,8 +627,25 @@ llsa_status llsa_kv_backward(const llsa_config* cfg, uint32_t units, llsa_dtype 
   NONNULL(flat);
   NONNULL(dk);
   NONNULL(dv);
-  if (!ws || ws_bytes < simt_backward_ws_bytes(g, units))
+  if (!ws || ws_bytes < backward_ws(g, units))
     return fail(LLSA_ERR_ARGUMENT, "backward workspace too small");
+  if (tc_supported(g, dt)) {
+    // the tensor-core backward also walks the query-major tables (and
+    // produces dq, here into scratch): rebuild the tables from the CSC lists
+    const TcStagedWs w(g, units);
+    char* p = static_cast<char*>(ws);
+    TcBuffers tb;
+    tc_carve(g, units, p, &tb);
+    cudaStream_t s = S(stream);
+    uint32_t* tables = reinterpret_cast<uint32_t*>(p + w.tcb + w.bwd);
+    if (llsa_status st = tables_from_csc(g, units, offs, flat, tables,
+                                         p + w.tcb + w.bwd + w.tab, s))
+      return st;
+    if (llsa_status st = tc_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
+    float* dq = reinterpret_cast<float*>(p + w.tcb + w.bwd + w.tab + w.cur);
+    return tc_backward(g, units, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, tables, offs, flat,
+                       dq, dk, dv, tb, p + w.tcb, s);
+  }
   return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, nullptr, offs,
                        flat, nullptr, dk, dv, ws, S(stream));
 }
@@ -696,6 +758,11 @@ struct llsa_handle_s {
   size_t tr_ws_bytes = 0;
   void* bwd_ws = nullptr;
   size_t bwd_ws_bytes = 0;
+  // bf16-output mode (llsa_handle_*_ex): fp32 results land here first; the
+  // backward reads O from out32 (D = rowsum(dO∘O) needs the fp32 output).
+  float* out32 = nullptr;      // [units][n][d]
+  float* grad32 = nullptr;     // dq | dk | dv, [3][units][n][d]
+  const void* last_out16 = nullptr;
   TcBuffers tcb;
   uint32_t last_launches = 0;
   size_t sizes[8] = {};
@@ -772,14 +839,149 @@ llsa_status llsa_handle_destroy(llsa_handle h) {
   delete h->timers[0];
   delete h->timers[1];
   if (h->arena) cudaFree(h->arena);
+  if (h->out32) cudaFree(h->out32);
+  if (h->grad32) cudaFree(h->grad32);
   delete h;
   return LLSA_OK;
 }
 
 int llsa_handle_uses_tensor_cores(llsa_handle h) { return h && h->tc ? 1 : 0; }
 
+}  // extern "C"
+
+static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* k,
+                                      const void* v, float* out, void* stream);
+static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const void* q,
+                                       const void* k, const void* v, const float* out,
+                                       float* dq, float* dk, float* dv, void* stream);
+
+namespace llsa_impl {
+namespace cvt {
+// fp32 → bf16 (RNE) of up to three equally sized tensors in one launch
+struct CvtArgs {
+  const float* src[3];
+  __nv_bfloat16* dst[3];
+  uint32_t count;
+  uint64_t n4;  // elements / 4 per tensor
+};
+__global__ void __launch_bounds__(256) to_bf16_kernel(CvtArgs a) {
+  const uint64_t total = a.n4 * a.count;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(i / a.n4);
+    const uint64_t j = i - t * a.n4;
+    const float4 x = __ldcs(reinterpret_cast<const float4*>(a.src[t]) + j);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&lo);
+    o.y = *reinterpret_cast<uint32_t*>(&hi);
+    __stcs(reinterpret_cast<uint2*>(a.dst[t]) + j, o);
+  }
+}
+}  // namespace cvt
+}  // namespace llsa_impl
+
+static llsa_status to_bf16(const float* const* src, void* const* dst, uint32_t count,
+                           size_t elems, cudaStream_t s) {
+  llsa_impl::cvt::CvtArgs a{};
+  for (uint32_t t = 0; t < count; ++t) {
+    a.src[t] = src[t];
+    a.dst[t] = static_cast<__nv_bfloat16*>(dst[t]);
+  }
+  a.count = count;
+  a.n4 = elems / 4;  // n·d is a multiple of 4 on every tensor-core shape (d = 64)
+  if (elems % 4) return fail(LLSA_ERR_UNSUPPORTED, "bf16 outputs need n*d %% 4 == 0");
+  llsa_impl::cvt::to_bf16_kernel<<<148 * 8, 256, 0, s>>>(a);
+  count_launch();
+  LLSA_LAUNCH_CHECK("to_bf16_kernel");
+  return LLSA_OK;
+}
+
+extern "C" {
+
 llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, const void* v,
                                 float* out, void* stream) {
+  return llsa_handle_forward_ex(h, q, k, v, out, LLSA_F32, stream);
+}
+
+llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q,
+                                 const void* k, const void* v, const float* out, float* dq,
+                                 float* dk, float* dv, void* stream) {
+  return llsa_handle_backward_ex(h, d_out, q, k, v, out, dq, dk, dv, LLSA_F32, stream);
+}
+
+static llsa_status ensure(float** p, size_t bytes) {
+  if (*p) return LLSA_OK;
+  if (cudaMalloc(reinterpret_cast<void**>(p), bytes) != cudaSuccess) {
+    *p = nullptr;
+    return fail(LLSA_ERR_CUDA, "cudaMalloc of %zu bytes failed", bytes);
+  }
+  return LLSA_OK;
+}
+
+llsa_status llsa_handle_forward_ex(llsa_handle h, const void* q, const void* k, const void* v,
+                                   void* out_user, llsa_dtype out_dtype, void* stream) {
+  NONNULL(h);
+  NONNULL(out_user);
+  if (llsa_status st = dtype_ok(out_dtype)) return st;
+  const size_t elems = (size_t)h->units * h->g.n * h->g.d;
+  float* out = static_cast<float*>(out_user);
+  if (out_dtype == LLSA_BF16) {
+    DeviceGuard dg(h->device);
+    if (llsa_status st = ensure(&h->out32, elems * 4)) return st;
+    out = h->out32;
+  }
+  llsa_status st = handle_forward_f32(h, q, k, v, out, stream);
+  if (!st && out_dtype == LLSA_BF16) {
+    DeviceGuard dg(h->device);
+    const float* src[3] = {h->out32, nullptr, nullptr};
+    void* dst[3] = {out_user, nullptr, nullptr};
+    st = to_bf16(src, dst, 1, elems, S(stream));
+    h->last_launches += 1;
+    h->last_out16 = out_user;
+  }
+  return st;
+}
+
+llsa_status llsa_handle_backward_ex(llsa_handle h, const void* d_out, const void* q,
+                                    const void* k, const void* v, const void* out_user,
+                                    void* dq, void* dk, void* dv, llsa_dtype out_dtype,
+                                    void* stream) {
+  NONNULL(h);
+  NONNULL(out_user);
+  NONNULL(dq);
+  NONNULL(dk);
+  NONNULL(dv);
+  if (llsa_status st = dtype_ok(out_dtype)) return st;
+  if (out_dtype == LLSA_F32)
+    return handle_backward_f32(h, d_out, q, k, v, static_cast<const float*>(out_user),
+                               static_cast<float*>(dq), static_cast<float*>(dk),
+                               static_cast<float*>(dv), stream);
+  if (!h->out32 || out_user != h->last_out16)
+    return fail(LLSA_ERR_STALE_STATE,
+                "bf16-output backward needs the bf16 output of this handle's latest forward");
+  const size_t elems = (size_t)h->units * h->g.n * h->g.d;
+  {
+    DeviceGuard dg(h->device);
+    if (llsa_status st = ensure(&h->grad32, 3 * elems * 4)) return st;
+  }
+  float* g = h->grad32;
+  llsa_status st = handle_backward_f32(h, d_out, q, k, v, h->out32, g, g + elems, g + 2 * elems,
+                                       stream);
+  if (!st) {
+    DeviceGuard dg(h->device);
+    const float* src[3] = {g, g + elems, g + 2 * elems};
+    void* dst[3] = {dq, dk, dv};
+    st = to_bf16(src, dst, 3, elems, S(stream));
+    h->last_launches += 1;
+  }
+  return st;
+}
+
+}  // extern "C"
+
+static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* k,
+                                      const void* v, float* out, void* stream) {
   NONNULL(h);
   DeviceGuard dg(h->device);
   NONNULL(q);
@@ -819,9 +1021,9 @@ llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k, con
   return st;
 }
 
-llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q,
-                                 const void* k, const void* v, const float* out, float* dq,
-                                 float* dk, float* dv, void* stream) {
+static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const void* q,
+                                       const void* k, const void* v, const float* out,
+                                       float* dq, float* dk, float* dv, void* stream) {
   NONNULL(h);
   DeviceGuard dg(h->device);
   NONNULL(d_out);
@@ -856,6 +1058,8 @@ llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q
   h->last_launches = take_launch_count();
   return st;
 }
+
+extern "C" {
 
 llsa_status llsa_handle_buffer(llsa_handle h, llsa_buffer which, void** ptr, size_t* bytes) {
   NONNULL(h);

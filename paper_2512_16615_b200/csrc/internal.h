@@ -100,6 +100,12 @@ llsa_status launch_transpose(const uint32_t* idx, uint64_t idx_unit_stride, uint
                              uint32_t* offsets, uint64_t off_unit_stride, uint32_t* flat,
                              uint64_t flat_unit_stride, void* ws, cudaStream_t s);
 
+// CSC → per-level selection tables (sorted rows), for kv_backward's tensor-core path.
+size_t tables_from_csc_ws(const Geometry& g, uint32_t units);
+llsa_status tables_from_csc(const Geometry& g, uint32_t units, const uint32_t* csc_offsets,
+                            const uint32_t* csc_flat, uint32_t* tables, void* ws,
+                            cudaStream_t s);
+
 llsa_status launch_build_plan(const Geometry& g, uint32_t units, const uint32_t* tables,
                               uint32_t* plan_level, uint32_t* plan_block,
                               float* plan_weight, cudaStream_t s);

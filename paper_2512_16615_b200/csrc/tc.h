@@ -39,6 +39,10 @@ llsa_status fused_pyramids(const Geometry& g, uint32_t units, const void* q, con
 size_t tc_buffer_bytes(const Geometry& g, uint32_t units);
 void tc_carve(const Geometry& g, uint32_t units, char* base, TcBuffers* out);
 
+// K'/V' = gain·pyramid as bf16 hi + lo from fp32 pyramids (the staged path;
+// the handle gets them from fused_pyramids).
+llsa_status tc_prep(const Geometry& g, uint32_t units, const float* pyr_k, const float* pyr_v,
+                    const TcBuffers& tb, cudaStream_t s);
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,

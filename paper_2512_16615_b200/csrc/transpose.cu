@@ -594,3 +594,97 @@ llsa_status mask_lookup(const Geometry& g, uint32_t units, const uint32_t* table
 }
 
 }  // namespace llsa_impl
+
+// ---------------------------------------------------------------------------
+// CSC → CSR: the per-level selection tables rebuilt from the key→query lists
+// (kv_backward receives only the transposed lists, attention_grad.hpp:32-37,
+// while the tensor-core backward walks the query-major tables as well).
+// Every query block appears K times per level; its row is filled by atomic
+// cursors and then sorted ascending (the tables' canonical order,
+// selection.cpp:37), so the result is deterministic.
+// ---------------------------------------------------------------------------
+namespace llsa_impl {
+namespace {
+
+__global__ void csc_scatter_kernel(const uint32_t* __restrict__ offs,
+                                   const uint32_t* __restrict__ flat, uint32_t units,
+                                   uint32_t key_blocks, uint32_t rows, uint32_t K,
+                                   uint64_t off_stride, uint64_t flat_stride,
+                                   uint64_t tab_stride, uint32_t* __restrict__ cursor,
+                                   uint32_t* __restrict__ tables, uint32_t* flag) {
+  const uint64_t total = (uint64_t)units * key_blocks;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = t / key_blocks, b = t - u * key_blocks;
+    const uint32_t* o = offs + u * off_stride;
+    const uint32_t s0 = o[b], s1 = o[b + 1];
+    if (s1 < s0 || s1 > rows * K) {
+      raise_flag(flag, kErrIndex);
+      continue;
+    }
+    for (uint32_t e = s0; e < s1; ++e) {
+      const uint32_t q = flat[u * flat_stride + e];
+      if (q >= rows) {
+        raise_flag(flag, kErrIndex);
+        continue;
+      }
+      const uint32_t pos = atomicAdd(&cursor[u * rows + q], 1u);
+      if (pos >= K) {
+        raise_flag(flag, kErrIndex);
+        continue;
+      }
+      tables[u * tab_stride + (uint64_t)q * K + pos] = (uint32_t)b;
+    }
+  }
+}
+
+__global__ void row_sort_kernel(uint32_t* __restrict__ tables, uint32_t units, uint32_t rows,
+                                uint32_t K, uint64_t tab_stride,
+                                const uint32_t* __restrict__ cursor, uint32_t* flag) {
+  const uint64_t total = (uint64_t)units * rows;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = t / rows, r = t - u * rows;
+    if (cursor[t] != K) raise_flag(flag, kErrIndex);  // a query block not listed K times
+    uint32_t* row = tables + u * tab_stride + r * K;
+    for (uint32_t i = 1; i < K; ++i) {
+      const uint32_t x = row[i];
+      uint32_t j = i;
+      for (; j > 0 && row[j - 1] > x; --j) row[j] = row[j - 1];
+      row[j] = x;
+    }
+  }
+}
+
+}  // namespace
+
+size_t tables_from_csc_ws(const Geometry& g, uint32_t units) {
+  size_t rows = 0;
+  for (uint32_t l = 0; l < g.L; ++l) rows += g.level_blocks(l);
+  return ((size_t)units * rows * 4 + 255) & ~size_t(255);
+}
+
+llsa_status tables_from_csc(const Geometry& g, uint32_t units, const uint32_t* offs,
+                            const uint32_t* flat, uint32_t* tables, void* ws, cudaStream_t s) {
+  uint32_t* cursor = static_cast<uint32_t*>(ws);
+  LLSA_CUDA_TRY(cudaMemsetAsync(cursor, 0, tables_from_csc_ws(g, units), s));
+  size_t crow = 0;
+  for (uint32_t l = 0; l < g.L; ++l) {
+    const uint32_t rows = (uint32_t)g.level_blocks(l);  // query blocks = key blocks per level
+    uint32_t* cur = cursor + (size_t)units * crow;
+    csc_scatter_kernel<<<grid_for((uint64_t)units * rows, 256), 256, 0, s>>>(
+        offs + g.csc_off_off[l], flat + g.csc_flat_off[l], units, rows, rows, g.K,
+        g.csc_off_entries, g.csc_flat_entries, g.table_entries, cur,
+        tables + g.table_off[l], device_flag());
+    count_launch();
+    LLSA_LAUNCH_CHECK("csc_scatter_kernel");
+    row_sort_kernel<<<grid_for((uint64_t)units * rows, 256), 256, 0, s>>>(
+        tables + g.table_off[l], units, rows, g.K, g.table_entries, cur, device_flag());
+    count_launch();
+    LLSA_LAUNCH_CHECK("row_sort_kernel");
+    crow += rows;
+  }
+  return LLSA_OK;
+}
+
+}  // namespace llsa_impl

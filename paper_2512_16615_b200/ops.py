@@ -576,37 +576,51 @@ class LLSAHandle:
             if t.device != self.device:
                 raise _lib.ArgumentError(f"{name} is on {t.device}, the handle on {self.device}")
 
-    def _check_outputs(self, **ts) -> None:
+    def _check_outputs(self, dtype=torch.float32, **ts) -> None:
         shape = (self.units, self.cfg.n, self.cfg.d)
         for name, t in ts.items():
-            if tuple(t.shape) != shape or t.dtype != torch.float32 or \
+            if tuple(t.shape) != shape or t.dtype != dtype or \
                     t.device != self.device or not t.is_contiguous():
-                raise _lib.ShapeMismatch(f"{name} must be a contiguous float32 {shape} tensor "
+                raise _lib.ShapeMismatch(f"{name} must be a contiguous {dtype} {shape} tensor "
                                          f"on {self.device}")
 
-    def forward(self, q, k, v, out=None):
+    @staticmethod
+    def _out_code(dtype: torch.dtype) -> int:
+        if dtype == torch.float32:
+            return _lib.F32
+        if dtype == torch.bfloat16:
+            return _lib.BF16
+        raise _lib.ArgumentError(f"outputs are float32 or bfloat16, not {dtype}")
+
+    def forward(self, q, k, v, out=None, out_dtype: torch.dtype | None = None):
+        """O = attention(q, k, v): [units, n, d] in `out_dtype` (float32 default;
+        bfloat16 halves the output bytes, llsa_handle_forward_ex)."""
         self._check_inputs(q=q, k=k, v=v)
         q, k, v = (t.contiguous() for t in (q, k, v))
-        out = out if out is not None else torch.empty(q.shape, device=q.device,
-                                                      dtype=torch.float32)
-        self._check_outputs(out=out)
+        out_dtype = out.dtype if out is not None else (out_dtype or torch.float32)
+        code = self._out_code(out_dtype)
+        out = out if out is not None else torch.empty(q.shape, device=q.device, dtype=out_dtype)
+        self._check_outputs(out_dtype, out=out)
         with torch.cuda.device(self.device):
-            check(self.lib.llsa_handle_forward(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
-                                               _stream()))
+            check(self.lib.llsa_handle_forward_ex(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                                  code, _stream()))
         return out
 
     def backward(self, d_out, q, k, v, out, dq=None, dk=None, dv=None):
+        """(dq, dk, dv) in the dtype of `out` (the forward's output)."""
         self._check_inputs(d_out=d_out, q=q, k=k, v=v)
         d_out, q, k, v = (t.contiguous() for t in (d_out, q, k, v))
-        mk = lambda: torch.empty(q.shape, device=q.device, dtype=torch.float32)  # noqa: E731
+        odt = out.dtype
+        code = self._out_code(odt)
+        mk = lambda: torch.empty(q.shape, device=q.device, dtype=odt)  # noqa: E731
         dq = dq if dq is not None else mk()
         dk = dk if dk is not None else mk()
         dv = dv if dv is not None else mk()
-        self._check_outputs(out=out, dq=dq, dk=dk, dv=dv)
+        self._check_outputs(odt, out=out, dq=dq, dk=dk, dv=dv)
         with torch.cuda.device(self.device):
-            check(self.lib.llsa_handle_backward(self._h, _ptr(d_out), _ptr(q), _ptr(k), _ptr(v),
-                                                _ptr(out), _ptr(dq), _ptr(dk), _ptr(dv),
-                                                _stream()))
+            check(self.lib.llsa_handle_backward_ex(self._h, _ptr(d_out), _ptr(q), _ptr(k),
+                                                   _ptr(v), _ptr(out), _ptr(dq), _ptr(dk),
+                                                   _ptr(dv), code, _stream()))
         return dq, dk, dv
 
 

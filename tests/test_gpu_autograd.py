@@ -50,3 +50,27 @@ def test_autograd_matches_handle_and_guards_staleness():
     attn(qs, ks, vs)                      # a newer forward on the same layer
     with pytest.raises(llsa.StaleState):
         y1.backward(g)
+
+
+def test_handle_bf16_outputs_are_rounded_fp32_outputs():
+    # llsa_handle_forward_ex / backward_ex with bf16 results: exactly the
+    # fp32 results rounded to bf16 (RNE); a backward against any other output
+    # buffer than the latest forward's raises StaleState
+    n = 16384
+    q, k, v, g = (torch.randn(2, n, 64, device="cuda").to(torch.bfloat16) for _ in range(4))
+    cfg = llsa.LLSAConfig(n, 64, 16, 8, 2, 2)
+    h = llsa.LLSAHandle(cfg, 2)
+    out32 = h.forward(q, k, v)
+    grads32 = h.backward(g, q, k, v, out32)
+    out16 = h.forward(q, k, v, out_dtype=torch.bfloat16)
+    assert out16.dtype == torch.bfloat16
+    assert torch.equal(out16, out32.to(torch.bfloat16))
+    grads16 = h.backward(g, q, k, v, out16)
+    for a, b in zip(grads16, grads32):
+        assert a.dtype == torch.bfloat16 and torch.equal(a, b.to(torch.bfloat16))
+    with pytest.raises(llsa.StaleState):
+        h.backward(g, q, k, v, out16.clone())
+    with pytest.raises(llsa.ShapeMismatch):
+        h.forward(q[:1], k[:1], v[:1])
+    with pytest.raises(llsa.ArgumentError):
+        h.forward(q.half(), k.half(), v.half())

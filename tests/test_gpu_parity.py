@@ -259,6 +259,10 @@ def _staged(oracle_c, cfg: Config, seed: int, bf: bool):
                          f"e{c.enrich_levels}m{c.reweight_mode}s{int(c.safe_softmax)}")
 @pytest.mark.parametrize("bf", [False, True])
 def test_staged_path_matches_oracle(oracle_c, cfg, bf):
+    # bf16 inputs at d = 64, B = 16 (safe softmax) run the tensor-core kernels
+    # behind the staged C ABI (the bf16 bar); everything else the fp32 SIMT
+    # kernels (rounding-level agreement)
+    tc = bf and cfg.d == 64 and cfg.block_size == 16 and cfg.safe_softmax
     ref, vc, (tq, tk, tv, tdo), pk, pv, tables = _staged(oracle_c, cfg, 100 + cfg.n, bf)
     np.testing.assert_array_equal(U32(tables[0]), ref.tables)
     lv, bl, w = llsa.build_plan(tables, vc)
@@ -266,23 +270,32 @@ def test_staged_path_matches_oracle(oracle_c, cfg, bf):
     np.testing.assert_array_equal(U32(bl[0]).reshape(-1), ref.plan_block)
     np.testing.assert_array_equal(w[0].cpu().numpy().reshape(-1), ref.plan_weight)
     st = llsa.llsa_forward(tq, tk, tv, pk, pv, tables, vc)
-    tol = 1e-4   # fp32 math on identical inputs: rounding-level agreement
+    tol = 2e-2 if tc else 1e-4   # fp32 math on identical inputs: rounding-level agreement
     assert rel_err(st.output[0].cpu().numpy(), ref.out)["max_rel"] <= tol
     np.testing.assert_allclose(lse(st.row_max[0].cpu().numpy(), st.row_denom[0].cpu().numpy()),
-                               lse(ref.row_max, ref.row_denom), rtol=1e-5, atol=1e-4)
+                               lse(ref.row_max, ref.row_denom),
+                               rtol=1e-5, atol=TOL_LSE if tc else 1e-4)
     tr = llsa.transpose_all(tables, vc)
     np.testing.assert_array_equal(U32(tr[0][0]), ref.csc_offsets)
     np.testing.assert_array_equal(U32(tr[1][0]), ref.csc_flat)
     dq, dk, dv = llsa.llsa_backward(tdo, st, tq, tk, tv, pk, pv, tables, tr, vc)
+    llsa.sync_status()
     for name, got, want in (("dq", dq, ref.dq), ("dk", dk, ref.dk), ("dv", dv, ref.dv)):
         e = rel_err(got[0].cpu().numpy(), want)
-        assert e["max_rel"] <= 1e-3, (name, e)
+        assert e["max_rel"] <= (2e-2 if tc else 1e-3), (name, e)
+    # kv_backward (CSC lists only; the tensor-core path rebuilds the tables)
+    # runs the same kernels: bit-identical dk, dv
     dk2, dv2 = llsa.kv_backward(tdo, st, tq, tk, tv, pk, pv, tr, vc)
+    llsa.sync_status()
     assert torch.equal(dk2, dk) and torch.equal(dv2, dv)
     # the mask-based baseline (oracle.cpp:365-501) finds the same key→query
-    # lists through dense block masks, so it reproduces the CSC path exactly
+    # lists through dense block masks (SIMT kernels): it reproduces the SIMT
+    # CSC path exactly, and the tensor-core one within the bf16 bar
     dk3, dv3 = llsa.mask_kv_backward(tdo, st, tq, tk, tv, pk, pv, tables, vc)
-    assert torch.equal(dk3, dk) and torch.equal(dv3, dv)
+    if tc:
+        assert rel_err(dk3[0].cpu().numpy(), ref.dk)["max_rel"] <= 2e-2
+    else:
+        assert torch.equal(dk3, dk) and torch.equal(dv3, dv)
 
 
 def test_forward_overflow_without_rescaling_raises():
