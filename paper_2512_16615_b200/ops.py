@@ -147,6 +147,17 @@ def _as_units(x: torch.Tensor, name: str) -> torch.Tensor:
     return x.contiguous()
 
 
+def _as_tables(x: torch.Tensor, cfg) -> torch.Tensor:
+    """Selection tables as [units, table_entries] int32 (1-D: one unit)."""
+    if not x.is_cuda:
+        raise _lib.ArgumentError("tables must be a CUDA tensor (no CPU path exists)")
+    x = x.reshape(1, -1) if x.dim() == 1 else x.reshape(x.shape[0], -1)
+    if x.shape[1] != cfg.table_entries:
+        raise _lib.ShapeMismatch(f"tables hold {x.shape[1]} entries per unit, the config "
+                                 f"{cfg.table_entries}")
+    return x.to(torch.int32).contiguous()
+
+
 def sync_status() -> None:
     """Synchronise and raise any device-detected error (llsa_sync_status)."""
     check(_lib.load().llsa_sync_status(C.c_void_p(_stream())))
@@ -338,7 +349,7 @@ def transpose_indices(idx: torch.Tensor, key_blocks: int) -> tuple:
 def transpose_all(tables: torch.Tensor, cfg: ValidatedConfig) -> tuple:
     """transpose_all, indexmap.hpp:36-37 → flat (offsets, flat) per unit."""
     lib = _lib.load()
-    t = _as_units(tables, "tables")
+    t = _as_tables(tables, cfg)
     units = t.shape[0]
     no = int(lib.llsa_csc_offsets_entries(C.byref(cfg.c())))
     nf = int(lib.llsa_csc_flat_entries(C.byref(cfg.c())))
@@ -360,7 +371,7 @@ def build_plan(tables: torch.Tensor, cfg: ValidatedConfig) -> tuple:
     """build_plan, attention.hpp:44-45 → (level, block, weight) each
     ``[units, fine_blocks, E]``."""
     lib = _lib.load()
-    t = _as_units(tables, "tables")
+    t = _as_tables(tables, cfg)
     units, E = t.shape[0], cfg.effective_blocks
     shape = (units, cfg.fine_blocks, E)
     lv = torch.empty(shape, device=t.device, dtype=torch.int32)
@@ -397,7 +408,9 @@ def llsa_forward(q, k, v, pyr_k, pyr_v, tables, cfg: ValidatedConfig,
     q, k, v = (_as_units(t, n) for t, n in ((q, "q"), (k, "k"), (v, "v")))
     _check_qkv(q, k, v, cfg)
     units = q.shape[0]
-    pk, pv, tb = _as_units(pyr_k, "pyr_k"), _as_units(pyr_v, "pyr_v"), _as_units(tables, "tables")
+    pk, pv, tb = _as_units(pyr_k, "pyr_k"), _as_units(pyr_v, "pyr_v"), _as_tables(tables, cfg)
+    if tb.shape[0] != units or pk.shape[0] != units or pv.shape[0] != units:
+        raise _lib.ShapeMismatch("tables / pyramids must cover the same units as q, k, v")
     out = torch.empty((units, cfg.n, cfg.d), device=q.device, dtype=torch.float32)
     rm = torch.empty((units, cfg.n), device=q.device, dtype=torch.float32)
     rd = torch.empty((units, cfg.n), device=q.device, dtype=torch.float32)
@@ -430,7 +443,7 @@ def llsa_backward(d_out, state: ForwardState, q, k, v, pyr_k, pyr_v, tables, tra
     check(lib.llsa_backward(C.byref(cfg.c()), units, _dtype_code(q), _ptr(dO), _ptr(out),
                             _ptr(state.row_max.contiguous()), _ptr(state.row_denom.contiguous()),
                             _ptr(q), _ptr(k), _ptr(v), _ptr(_as_units(pyr_k, "pyr_k")),
-                            _ptr(_as_units(pyr_v, "pyr_v")), _ptr(_as_units(tables, "tables")),
+                            _ptr(_as_units(pyr_v, "pyr_v")), _ptr(_as_tables(tables, cfg)),
                             _ptr(offs.contiguous()), _ptr(flat.contiguous()), _ptr(dq), _ptr(dk),
                             _ptr(dv), _ptr(ws), wsb, _stream()))
     return dq, dk, dv
@@ -480,7 +493,7 @@ def mask_kv_backward(d_out, state: ForwardState, q, k, v, pyr_k, pyr_v, tables,
                                     _ptr(state.row_denom.contiguous()), _ptr(q),
                                     _ptr(_as_units(pyr_k, "pyr_k")),
                                     _ptr(_as_units(pyr_v, "pyr_v")), _ptr(k), _ptr(v),
-                                    _ptr(tables.contiguous()), _ptr(dk), _ptr(dv), _ptr(ws), wsb,
+                                    _ptr(_as_tables(tables, cfg)), _ptr(dk), _ptr(dv), _ptr(ws), wsb,
                                     _stream()))
     return dk, dv
 

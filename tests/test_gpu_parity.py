@@ -478,3 +478,32 @@ def test_multi_unit_handle_is_per_unit_exact(n, L):
         for a, b in zip(grads, g1):
             assert torch.equal(a[sl], b), u
     llsa.sync_status()
+
+
+@pytest.mark.parametrize("n,L", [(16384, 2), (65536, 3)])
+def test_staged_tensor_core_path_equals_handle(n, L):
+    # the reference-shaped staged C ABI (bf16) runs the handle's kernels:
+    # tables, CSC lists, forward and backward bit-identical, 2 units
+    units = 2
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
+                   for _ in range(4))
+    cfg = llsa.LLSAConfig(n, 64, 16, 8, L, L)
+    vc = llsa.validate_config(cfg)
+    h = llsa.LLSAHandle(cfg, units)
+    o = h.forward(q, k, v)
+    grads = h.backward(dO, q, k, v, o)
+    pq, pk, pv = (llsa.build_pyramid(t, 16, L) for t in (q, k, v))
+    tables = llsa.hierarchical_topk(pq, pk, vc)
+    assert torch.equal(tables.view(-1), h.view("tables").view(-1))
+    st = llsa.llsa_forward(q, k, v, pk, pv, tables, vc)
+    assert torch.equal(st.output, o)
+    tr = llsa.transpose_all(tables, vc)
+    assert torch.equal(tr[0].view(-1), h.view("csc_offsets").view(-1))
+    assert torch.equal(tr[1].view(-1), h.view("csc_flat").view(-1))
+    sg = llsa.llsa_backward(dO, st, q, k, v, pk, pv, tables, tr, vc)
+    for a, b in zip(sg, grads):
+        assert torch.equal(a, b)
+    dk, dv = llsa.kv_backward(dO, st, q, k, v, pk, pv, tr, vc)
+    llsa.sync_status()
+    assert torch.equal(dk, grads[1]) and torch.equal(dv, grads[2])
