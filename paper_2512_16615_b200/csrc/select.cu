@@ -184,6 +184,76 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
   return d;
 }
 
+// Top-K of each of the block's B query rows from scores[r * 256 + c] (one
+// warp per row; lane owns positions lane*PL .. lane*PL+PL-1): K rounds of a
+// warp arg-max over order-preserving keys (score desc, position asc), then
+// the kept ids in position order (sorted when the parent row was not).
+template <int PL>
+__device__ __forceinline__ void topk_rows(const float* scores, const uint32_t* ids, uint32_t C,
+                                          uint32_t K, uint32_t B, uint32_t* out_blk,
+                                          bool asc) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t r = warp; r < B; r += blockDim.x >> 5) {
+    // lane owns positions lane*PL .. lane*PL+PL-1 (contiguous, so position
+    // order = (lane, i) order; PL = 4 covers C <= 128 with every lane busy).
+    // Scores become order-preserving u32 keys (-0 → +0, the float compare
+    // ties them); each round takes the warp max key with redux.sync and,
+    // among equal keys, the lowest position (topk_row's lowest-index
+    // tie-break), so the selection is exact.
+    uint32_t key[PL];
+    uint32_t taken = 0;
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+      const uint32_t c = lane * PL + i;
+      float v = c < C ? scores[r * 256 + c] : 0.f;
+      if (v == 0.f) v = 0.f;  // canonical +0
+      const uint32_t u = __float_as_uint(v);
+      key[i] = c < C ? ((u & 0x80000000u) ? ~u : (u | 0x80000000u)) : 0u;  // valid keys > 0
+    }
+    for (uint32_t round = 0; round < K; ++round) {
+      uint32_t lk = key[0], li = 0;
+#pragma unroll
+      for (int i = 1; i < PL; ++i)
+        if (key[i] > lk) {
+          lk = key[i];
+          li = i;
+        }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, lk);
+      const uint32_t mypos = lk == mk && lk != 0u ? lane * PL + li : 0xffffffffu;
+      const uint32_t bpos = __reduce_min_sync(0xffffffffu, mypos);
+      if (bpos == mypos) {
+        taken |= 1u << li;
+#pragma unroll
+        for (int i = 0; i < PL; ++i)
+          if ((uint32_t)i == li) key[i] = 0u;
+      }
+    }
+    const uint32_t cnt = __popc(taken);
+    uint32_t pre = cnt;  // inclusive scan of counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= (uint32_t)o) pre += y;
+    }
+    uint32_t pos = pre - cnt;
+    uint32_t* o = out_blk + (uint64_t)r * K;
+#pragma unroll
+    for (int i = 0; i < PL; ++i)
+      if ((taken >> i) & 1u) o[pos++] = ids[lane * PL + i];
+    if (!asc) {  // parent row out of order (user-built): rank-sort the K ids
+      __syncwarp();
+      const uint32_t x = lane < K ? o[lane] : 0u;
+      uint32_t rank = 0;
+      for (uint32_t j = 0; j < K; ++j) {
+        const uint32_t y = __shfl_sync(0xffffffffu, x, j);
+        rank += (y < x || (y == x && j < lane)) ? 1u : 0u;
+      }
+      __syncwarp();
+      if (lane < K) o[rank] = x;
+    }
+  }
+}
+
 // Fast variant for d % 4 == 0, B = 16 query rows per block, C = K·B <= 256
 // candidates, K <= 32: thread (row r, lane group cg) scores candidates
 // cg, cg+16, … with q_r and the candidate rows streamed as float4 from smem
@@ -281,67 +351,87 @@ __global__ void __launch_bounds__(256, 4) select_level_fast_kernel(
     }
   }
   __syncthreads();
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t r = warp; r < B; r += blockDim.x >> 5) {
-    // lane owns positions lane*PL .. lane*PL+PL-1 (contiguous, so position
-    // order = (lane, i) order; PL = 4 covers C <= 128 with every lane busy).
-    // Scores become order-preserving u32 keys (-0 → +0, the float compare
-    // ties them); each round takes the warp max key with redux.sync and,
-    // among equal keys, the lowest position (topk_row's lowest-index
-    // tie-break), so the selection is exact.
-    constexpr int PL = CPT / 2;
-    uint32_t key[PL];
-    uint32_t taken = 0;
-#pragma unroll
-    for (int i = 0; i < PL; ++i) {
-      const uint32_t c = lane * PL + i;
-      float v = c < C ? scores[r * 256 + c] : 0.f;
-      if (v == 0.f) v = 0.f;  // canonical +0
-      const uint32_t u = __float_as_uint(v);
-      key[i] = c < C ? ((u & 0x80000000u) ? ~u : (u | 0x80000000u)) : 0u;  // valid keys > 0
+  topk_rows<CPT / 2>(scores, ids, C, K, B, out + unit * out_unit_stride + (uint64_t)blk * B * K,
+                     asc);
+}
+
+// Register-blocked scorer for the hot shape (B = 16, d = 64, C = K·B <= 256):
+// thread = candidate, all 16 query rows of the block in registers (16 rows ×
+// two packed fp32x2 accumulators).  Per float4 step the thread loads its
+// candidate's 16 bytes once (distinct per lane, 4 wavefronts per warp) and
+// the 16 query float4s as warp-wide broadcasts, then issues 64 packed exact
+// multiply / add instructions: the candidate row is reused 16 times from a
+// register instead of being re-read per (row, candidate) pair, so the FP32
+// pipe, not shared memory, is the limit.  Same per-pair operations and order
+// as detail::dot (bit-exact scores); same top-K as above.
+template <int NT>
+__global__ void __launch_bounds__(NT) select_level_rb_kernel(
+    const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
+    uint64_t k_unit_stride, const uint32_t* __restrict__ parent, uint64_t parent_unit_stride,
+    uint32_t parent_k, uint32_t key_blocks, uint32_t K, float scale,
+    uint32_t* __restrict__ out, uint64_t out_unit_stride, uint32_t* flag, uint64_t negzero2) {
+  constexpr uint32_t B = 16, D = 64, LD = D + 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t blk = blockIdx.x, unit = blockIdx.y, tid = threadIdx.x;
+  const uint32_t C = parent_k * B;
+  uint32_t* ids = reinterpret_cast<uint32_t*>(smem);      // 256
+  float* scores = reinterpret_cast<float*>(ids + 256);    // 16 × 256
+  float* sq = scores + 16 * 256;                          // 16 × 64
+  float* sk = sq + 16 * D;                                // C × LD
+  const uint32_t* prow = parent + unit * parent_unit_stride + (uint64_t)blk * parent_k;
+  for (uint32_t c = tid; c < C; c += NT) {
+    uint32_t pb = prow[c / B];
+    if (pb >= key_blocks) {
+      raise_flag(flag, kErrIndex);
+      pb = 0;
     }
-    for (uint32_t round = 0; round < K; ++round) {
-      uint32_t lk = key[0], li = 0;
+    ids[c] = pb * B + c % B;
+  }
+  const uint32_t sq_s = (uint32_t)__cvta_generic_to_shared(sq);
+  const float* qu = q + unit * q_unit_stride + (uint64_t)blk * B * D;
+  for (uint32_t e = tid; e < B * D / 4; e += NT)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sq_s + e * 16),
+                 "l"(qu + 4 * e)
+                 : "memory");
+  const bool asc = __syncthreads_and(row_ascending(prow, parent_k)) != 0;
+  const float* ku = k + unit * k_unit_stride;
+  const uint32_t sk_s = (uint32_t)__cvta_generic_to_shared(sk);
+  for (uint32_t e = tid; e < C * (D / 4); e += NT) {
+    const uint32_t c = e >> 4, j = e & 15;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sk_s + (c * LD + 4 * j) * 4),
+                 "l"(ku + (uint64_t)ids[c] * D + 4 * j)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  if (tid < C) {
+    uint64_t acc[B][2];
 #pragma unroll
-      for (int i = 1; i < PL; ++i)
-        if (key[i] > lk) {
-          lk = key[i];
-          li = i;
-        }
-      const uint32_t mk = __reduce_max_sync(0xffffffffu, lk);
-      const uint32_t mypos = lk == mk && lk != 0u ? lane * PL + li : 0xffffffffu;
-      const uint32_t bpos = __reduce_min_sync(0xffffffffu, mypos);
-      if (bpos == mypos) {
-        taken |= 1u << li;
+    for (int r = 0; r < (int)B; ++r) acc[r][0] = acc[r][1] = 0ull;
+    const ulonglong2* kr = reinterpret_cast<const ulonglong2*>(sk + tid * LD);
+    const ulonglong2* qr = reinterpret_cast<const ulonglong2*>(sq);
 #pragma unroll
-        for (int i = 0; i < PL; ++i)
-          if ((uint32_t)i == li) key[i] = 0u;
+    for (int j = 0; j < (int)(D / 4); ++j) {
+      const ulonglong2 y = kr[j];
+#pragma unroll
+      for (int r = 0; r < (int)B; ++r) {
+        const ulonglong2 x = qr[r * (D / 4) + j];  // same address in every lane: broadcast
+        acc[r][0] = add2(acc[r][0], mul2_exact(x.x, y.x, negzero2));
+        acc[r][1] = add2(acc[r][1], mul2_exact(x.y, y.y, negzero2));
       }
     }
-    const uint32_t cnt = __popc(taken);
-    uint32_t pre = cnt;  // inclusive scan of counts
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= (uint32_t)o) pre += y;
-    }
-    uint32_t pos = pre - cnt;
-    uint32_t* o = out + unit * out_unit_stride + ((uint64_t)blk * B + r) * K;
-#pragma unroll
-    for (int i = 0; i < PL; ++i)
-      if ((taken >> i) & 1u) o[pos++] = ids[lane * PL + i];
-    if (!asc) {  // parent row out of order (user-built): rank-sort the K ids
-      __syncwarp();
-      const uint32_t x = lane < K ? o[lane] : 0u;
-      uint32_t rank = 0;
-      for (uint32_t j = 0; j < K; ++j) {
-        const uint32_t y = __shfl_sync(0xffffffffu, x, j);
-        rank += (y < x || (y == x && j < lane)) ? 1u : 0u;
-      }
-      __syncwarp();
-      if (lane < K) o[rank] = x;
+    for (int r = 0; r < (int)B; ++r) {
+      const float s0 = __uint_as_float((uint32_t)acc[r][0]);
+      const float s1 = __uint_as_float((uint32_t)(acc[r][0] >> 32));
+      const float s2 = __uint_as_float((uint32_t)acc[r][1]);
+      const float s3 = __uint_as_float((uint32_t)(acc[r][1] >> 32));
+      scores[r * 256 + tid] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
     }
   }
+  __syncthreads();
+  topk_rows<NT / 32>(scores, ids, C, K, B, out + unit * out_unit_stride + (uint64_t)blk * B * K,
+                     asc);
 }
 
 }  // namespace
@@ -379,6 +469,19 @@ llsa_status launch_select_level(const float* q, uint64_t q_unit_stride, const fl
     const size_t smem = 4 * (256 + 16 * 256 + 16 * ld + C * ld);
     if (smem <= 200 * 1024) {
       const uint32_t key_blocks = (uint32_t)(k_rows / B);
+      if (d == 64) {  // the hot shape: register-blocked scorer
+        const size_t smem_rb = 4 * (256 + 16 * 256 + 16 * 64 + C * 68);
+        auto rb = C <= 128 ? select_level_rb_kernel<128> : select_level_rb_kernel<256>;
+        if (smem_rb > 48 * 1024)
+          LLSA_CUDA_TRY(cudaFuncSetAttribute(rb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem_rb));
+        rb<<<dim3(parent_rows, units), C <= 128 ? 128 : 256, smem_rb, s>>>(
+            q, q_unit_stride, k, k_unit_stride, parent, parent_unit_stride, parent_k,
+            key_blocks, K, scale, out, out_unit_stride, device_flag(), 0x8000000080000000ull);
+        count_launch();
+        LLSA_LAUNCH_CHECK("select_level_rb_kernel");
+        return LLSA_OK;
+      }
       auto kern = C <= 128 ? select_level_fast_kernel<8> : select_level_fast_kernel<16>;
       if (smem > 48 * 1024)
         LLSA_CUDA_TRY(
