@@ -66,3 +66,57 @@ def test_reference_suite_on_gpu(suite):
     unexpected = failed - FP32_TOLERANCE_CASES.get(suite, set())
     assert not unexpected, r.stdout[-6000:]
     assert passed
+
+
+# ---------------------------------------------------------------------------
+# The reference's acceptance gate and its oracle-equivalence harness
+# (P/tests/acceptance.cpp A1-A9 and P/src/bench.cpp run_verify, both
+# unmodified) built against the drop-in (oracle/Makefile `acceptance`).
+# tests/golden/ref_f32_acceptance.txt is the same gate on the reference's own
+# f32 library: it fails A1 and A2 (1e-10 limits) and aborts A3 (finite
+# differences throw PrecisionError below double precision) — the allowlist.
+# (A6 is a wall-clock criterion; the f32 reference itself missed its spread
+# limit on the 8-vCPU build host, so it is not in the allowlist: the drop-in
+# must pass it.)
+FP32_ACCEPTANCE_ALLOWED = {"A1", "A2", "A3"}
+
+
+def _golden(name):
+    with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+        return f.read()
+
+
+def test_f32_reference_gate_allowlist_is_recorded():
+    g = _golden("ref_f32_acceptance.txt")
+    failed = set(re.findall(r"^\[FAIL\] (A\d)", g, flags=re.M))
+    assert FP32_ACCEPTANCE_ALLOWED <= failed
+    assert re.search(r"^\[FAIL\] A3 aborted: finite differences need the double", g, re.M)
+    assert "0 failed" in _golden("ref_f32_run_verify.txt")
+
+
+@pytest.mark.gpu
+def test_run_verify_on_drop_in():
+    exe = os.path.join(RT, "run_verify")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance harness not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    names = re.findall(r"^\[PASS\] (\S+)", r.stdout, flags=re.M)
+    assert r.returncode == 0, r.stdout
+    assert set(names) >= {"forward-oracle-scalekv", "forward-oracle-logitbias",
+                          "forward-dense-reduction", "transpose-mask-equivalence",
+                          "transpose-roundtrip", "backward-mask-scalekv",
+                          "backward-mask-logitbias", "negative-control"}
+
+
+@pytest.mark.gpu
+def test_acceptance_gate_on_drop_in():
+    exe = os.path.join(RT, "acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance harness not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
+    print(r.stdout)
+    passed = set(re.findall(r"^\[PASS\] (A\d)", r.stdout, flags=re.M))
+    failed = set(re.findall(r"^\[FAIL\] (A\d)", r.stdout, flags=re.M))
+    assert failed <= FP32_ACCEPTANCE_ALLOWED, r.stdout
+    assert passed >= {"A4", "A5", "A6", "A7", "A8", "A9"}, r.stdout
