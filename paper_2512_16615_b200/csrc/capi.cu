@@ -655,7 +655,7 @@ size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 size_t mask_kv_ws(const Geometry& g, uint32_t units) {
   return al256((size_t)units * g.csc_off_entries * 4) +
          al256((size_t)units * g.csc_flat_entries * 4) + al256(mask_lookup_ws_bytes(g, units)) +
-         al256(simt_backward_ws_bytes(g, units));
+         al256(backward_ws(g, units));
 }
 }  // namespace
 
@@ -697,6 +697,16 @@ llsa_status llsa_mask_kv_backward(const llsa_config* cfg, uint32_t units, llsa_d
   void* mws = p;
   p += al256(mask_lookup_ws_bytes(g, units));
   if (llsa_status st = mask_lookup(g, units, tables, offs, flat, mws, S(stream))) return st;
+  if (tc_supported(g, dt)) {  // the same tensor-core kernels as llsa_kv_backward
+    const TcStagedWs w(g, units);
+    TcBuffers tb;
+    tc_carve(g, units, p, &tb);
+    cudaStream_t s = S(stream);
+    if (llsa_status st = tc_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
+    float* dq = reinterpret_cast<float*>(p + w.tcb + w.bwd + w.tab + w.cur);
+    return tc_backward(g, units, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, tables, offs, flat,
+                       dq, dk, dv, tb, p + w.tcb, s);
+  }
   return simt_backward(g, units, dt, d_out, out, rm, rd, q, k, v, pyr_k, pyr_v, nullptr, offs,
                        flat, nullptr, dk, dv, p, S(stream));
 }
