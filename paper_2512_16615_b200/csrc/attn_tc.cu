@@ -2775,7 +2775,7 @@ constexpr int kStage = 38912;                  // 38 KB, 1024-aligned
 constexpr int kRing = 5;
 constexpr int kOffB = kRing * kStage;          // 190 KB: B' x 2 (16 KB each)
 constexpr int kOffInfo = kOffB + 2 * 16384;    // per-stage chunk facts
-constexpr int kFactSlots = 8, kFactWords = 36;  // item facts ring: lo, hi, ids[32]
+constexpr int kFactSlots = 16, kFactWords = 36;  // item facts ring: lo, hi, unit, kb, ids[32]
 constexpr int kOffFacts = kOffInfo + 64;
 constexpr int kOffBar = kOffFacts + kFactSlots * kFactWords * 4;
 constexpr int kAB = 4;  // Acc buffers (items in flight between MMA and epilogue)
@@ -2824,7 +2824,7 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     }
     for (int i = 0; i < kFactSlots; ++i) {
       mbar_init(bar(FACTF + i), 1);
-      mbar_init(bar(FACTE + i), 4);  // the four gather warps
+      mbar_init(bar(FACTE + i), 8);  // the four gather warps + the four epilogue warps
     }
     fence_mbar_init();
   }
@@ -3078,19 +3078,30 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
     // unrolling grew the kernel past what the instruction cache holds)
     constexpr int kEL = 4;  // coarse level slots on this path (L <= 4)
     struct EpiFacts {
-      uint32_t o0, o1;
+      uint32_t o0, o1, unit, kb;
       float v[kEL];
     };
-    auto issue = [&](uint64_t id, EpiFacts& f) {
+    // Item facts come from the facts warp's smem ring (segment bounds, unit,
+    // key block: no dependent global load, no 64-bit division); only the
+    // coarse adjoint values are global loads, issued two items ahead.
+    const uint32_t* fact = reinterpret_cast<const uint32_t*>(smem + kOffFacts);
+    auto issue = [&](uint32_t it, EpiFacts& f) {
       f.o0 = f.o1 = 0;
+      f.unit = 0;
+      f.kb = 0;
 #pragma unroll
       for (int sl = 0; sl < kEL; ++sl) f.v[sl] = 0.f;
-      if (id >= total) return;
-      const uint32_t unit = (uint32_t)(id / nkb);
-      const uint64_t kb = id % nkb;
-      const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[0];
-      f.o0 = off[kb];
-      f.o1 = off[kb + 1];
+      if (blockIdx.x + (uint64_t)it * gridDim.x >= total) return;
+      const uint32_t fs = it % kFactSlots;
+      mbar_wait(bar(FACTF + fs), (it / kFactSlots) & 1);
+      f.o0 = fact[fs * kFactWords];
+      f.o1 = fact[fs * kFactWords + 1];
+      f.unit = fact[fs * kFactWords + 2];
+      f.kb = fact[fs * kFactWords + 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(FACTE + fs));
+      const uint32_t unit = f.unit;
+      const uint64_t kb = f.kb;
 #pragma unroll
       for (int sl = 0; sl < kEL; ++sl) {
         if (sl < (int)p.ncl) {
@@ -3102,13 +3113,13 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       }
     };
     uint32_t ai = 0;
-    auto body = [&](uint64_t id, const EpiFacts& f) {
+    auto body = [&](const EpiFacts& f) {
       const uint32_t m = f.o1 - f.o0;
       float add = 0.f;
 #pragma unroll
       for (int sl = 0; sl < kEL; ++sl) add += f.v[sl];
-      const uint32_t unit = (uint32_t)(id / nkb);
-      const uint64_t kb = id % nkb;
+      const uint32_t unit = f.unit;
+      const uint64_t kb = f.kb;
       float acc[16];
       if (m) {
         const uint32_t ab = ai % kAB;
@@ -3133,14 +3144,18 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
       for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
     };
     const uint64_t G = gridDim.x;
-    EpiFacts fa, fb;
-    issue(blockIdx.x, fa);
-    for (uint64_t id = blockIdx.x; id < total; id += 2 * G) {
-      issue(id + G, fb);
-      body(id, fa);
-      if (id + G >= total) break;
-      issue(id + 2 * G, fa);
-      body(id + G, fb);
+    EpiFacts fa, fb, fc;  // items it, it+1, it+2 (unrolled by three: no register moves)
+    issue(0, fa);
+    issue(1, fb);
+    for (uint32_t it = 0; blockIdx.x + (uint64_t)it * G < total; it += 3) {
+      issue(it + 2, fc);
+      body(fa);
+      if (blockIdx.x + (uint64_t)(it + 1) * G >= total) break;
+      issue(it + 3, fa);
+      body(fb);
+      if (blockIdx.x + (uint64_t)(it + 2) * G >= total) break;
+      issue(it + 4, fb);
+      body(fc);
     }
   }
   fence_before();
