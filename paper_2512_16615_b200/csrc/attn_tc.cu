@@ -90,7 +90,7 @@ struct TcParams {
   // tcgen05 row-major coarse dK/dV (levels 1..lim-1): one task per
   // (level, selection row, query slice, 8-block key group)
   float* rpart;                           // row partials
-  uint32_t rows_on, groups;               // path enabled; key groups per row (K/8)
+  uint32_t rows_on, groups;               // path enabled; key groups per row (ceil(K/8))
   uint32_t rl_count;                      // levels handled (1..lim-1)
   uint32_t rl_level[kMaxLevels + 2];
   uint32_t rl_slices[kMaxLevels + 2];     // query slices per row
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(256, rows::Layout<LO>::kMinBlocks)
   // key group: 8 selected blocks × 16 rows of K', V' (hi [, lo])
   for (uint32_t i = tid; i < 8 * 16 * 8; i += blockDim.x) {
     const uint32_t key = i >> 3, ch = i & 7;
-    uint32_t b = trow[key >> 4];
+    uint32_t b = group * 8 + (key >> 4) < p.K ? trow[key >> 4] : 0u;  // dummy tail keys
     if (b >= nblk) b = 0;
     const uint64_t grow = p.pyr_off[level] + (uint64_t)b * kBS + (key & 15);
     const uint64_t src = pyr_off + grow * kD + ch * 8;
@@ -3285,6 +3285,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       uint32_t unit, slice, group;
       uint64_t row;
       decode(id, unit, row, slice, group);
+      // K not a multiple of 8: the last group's tail lanes gather block 0 as
+      // dummy keys; their dK'/dV' rows are never read by rows_reduce_kernel
+      if (group * 8 + lane >= p.K) return 0u;
       return p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K +
                       group * 8 + lane];
     };
@@ -3502,7 +3505,7 @@ uint32_t coarse_entries(const Geometry& g) {
 // selection width is a multiple of 8 blocks (one 128-key group = M).
 bool rows_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
-  return !(e && e[0] == '1') && g.enrich_lim() >= 2 && g.K % 8 == 0;
+  return !(e && e[0] == '1') && g.enrich_lim() >= 2;
 }
 
 // tcgen05 forward: every coarse entry's scores fit the TMEM S block
@@ -3534,7 +3537,7 @@ bool dqf_path(const Geometry& g) {
 void rows_layout(const Geometry& g, TcParams& P) {
   P.rows_on = rows_path(g) ? 1u : 0u;
   P.rl_count = 0;
-  P.groups = g.K / 8;
+  P.groups = (g.K + 7) / 8;  // a last partial group carries dummy keys (block 0)
   uint64_t tasks = 0, off = 0;
   if (P.rows_on) {
     for (uint32_t l = 1; l < g.enrich_lim(); ++l) {
