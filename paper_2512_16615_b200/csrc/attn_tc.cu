@@ -2957,8 +2957,10 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         if (info[s] & 0x400u) break;
         trace_ev(p, 3, c, 0);
         if (c >= 2) mbar_wait(bar(SFREE + b), ((c >> 1) - 1) & 1);
+        trace_ev(p, 3, c, 2);
         fence_proxy_async();  // the gather's cp.async writes → the MMA's async proxy
         fence_after();
+        trace_ev(p, 3, c, 3);
         const uint32_t st = sbase + s * kStage;
         const uint32_t tS = tmem + 32 * b, tP = tS + 16;
 #pragma unroll
@@ -2992,8 +2994,10 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
         mbar_wait(bar(BREADY + b), (c >> 1) & 1);
         trace_ev(p, 6, c, 1);
         if (first && ai >= (uint32_t)kAB) mbar_wait(bar(AFREE + ab), ((ai / kAB) - 1) & 1);
+        trace_ev(p, 6, c, 3);
         fence_proxy_async();
         fence_after();
+        trace_ev(p, 6, c, 4);
         const uint32_t st = sbase + s * kStage;
         const uint32_t sb = sbase + kOffB + b * 16384;
         const uint32_t ta = tmem + 64 + 64 * ab;

@@ -1,0 +1,74 @@
+// Microbenchmark (development tool, not part of the library): issue cost and
+// completion time of back-to-back tcgen05.mma kind::f16 (SS operands, SW128
+// K-major) by one thread, for M = 128 and several N.  One CTA per SM (grid
+// 148) so every SM's tensor core is measured under the same load.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/umma_bench
+//        tools/umma_bench.cu -I paper_2512_16615_b200/csrc
+#include <cstdint>
+#include <cstdio>
+
+#include "umma.cuh"
+
+using namespace llsa_umma;
+
+__global__ void __launch_bounds__(128) umma_bench(int N, int reps, int a_mn,
+                                                  unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sbase = (base + 1023) & ~1023u;
+  for (uint32_t i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem + (sbase - base))[i] = 0x3f803f80u;  // bf16 1.0
+  if (warp == 0) tmem_alloc((uint32_t)__cvta_generic_to_shared(&slot), 512);
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(mb, 1);
+    fence_mbar_init();
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, N, a_mn != 0, false);
+    const uint32_t sa = sbase, sb = sbase + 32768;
+    unsigned long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint64_t ad = a_mn ? desc_mnmajor(sa + (r & 3) * kKStepMNMajor, 16384)
+                               : desc_kmajor(sa + (r & 3) * kKStepKMajor);
+      mma_bf16(tmem, ad, desc_kmajor(sb + (r & 3) * kKStepKMajor), idesc, r > 0);
+    }
+    unsigned long long t1 = clock64();
+    commit(mb);
+    mbar_wait(mb, 0);
+    unsigned long long t2 = clock64();
+    if (blockIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(umma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  for (int a_mn = 0; a_mn < 2; ++a_mn)
+    for (int N : {16, 32, 64, 128, 256}) {
+      const int reps = 256;
+      unsigned long long h[2];
+      for (int w = 0; w < 2; ++w) umma_bench<<<148, 128, 66 * 1024>>>(N, reps, a_mn, d);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+      printf("M=128 N=%3d K=16 A=%s: issue %.1f cyc/mma, complete %.1f cyc/mma  (%s)\n", N,
+             a_mn ? "MN" : "K ", (double)h[0] / reps, (double)h[1] / reps,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
