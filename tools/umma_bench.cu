@@ -11,6 +11,16 @@
 
 using namespace llsa_umma;
 
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// a_mn: 0 = A K-major in smem, 1 = A MN-major in smem, 2 = A in TMEM (TS mode)
 __global__ void __launch_bounds__(128) umma_bench(int N, int reps, int a_mn,
                                                   unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -33,13 +43,18 @@ __global__ void __launch_bounds__(128) umma_bench(int N, int reps, int a_mn,
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = idesc_bf16(128, N, a_mn != 0, false);
+    const uint32_t idesc = idesc_bf16(128, N, a_mn == 1, false);
     const uint32_t sa = sbase, sb = sbase + 32768;
     unsigned long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      const uint64_t ad = a_mn ? desc_mnmajor(sa + (r & 3) * kKStepMNMajor, 16384)
-                               : desc_kmajor(sa + (r & 3) * kKStepKMajor);
-      mma_bf16(tmem, ad, desc_kmajor(sb + (r & 3) * kKStepKMajor), idesc, r > 0);
+      if (a_mn == 2) {  // D in columns [0, 256), A in columns [256 + 8*(r&3), ...)
+        mma_bf16_ts(tmem, tmem + 256 + 8 * (r & 3), desc_kmajor(sb + (r & 3) * kKStepKMajor),
+                    idesc, r > 0);
+      } else {
+        const uint64_t ad = a_mn ? desc_mnmajor(sa + (r & 3) * kKStepMNMajor, 16384)
+                                 : desc_kmajor(sa + (r & 3) * kKStepKMajor);
+        mma_bf16(tmem, ad, desc_kmajor(sb + (r & 3) * kKStepKMajor), idesc, r > 0);
+      }
     }
     unsigned long long t1 = clock64();
     commit(mb);
@@ -59,15 +74,16 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(umma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  for (int a_mn = 0; a_mn < 2; ++a_mn)
+  for (int a_mn = 0; a_mn < 3; ++a_mn)
     for (int N : {16, 32, 64, 128, 256}) {
+      if (a_mn == 2 && N > 256 - 0) continue;
       const int reps = 256;
       unsigned long long h[2];
       for (int w = 0; w < 2; ++w) umma_bench<<<148, 128, 66 * 1024>>>(N, reps, a_mn, d);
       cudaDeviceSynchronize();
       cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
       printf("M=128 N=%3d K=16 A=%s: issue %.1f cyc/mma, complete %.1f cyc/mma  (%s)\n", N,
-             a_mn ? "MN" : "K ", (double)h[0] / reps, (double)h[1] / reps,
+             a_mn == 2 ? "TMEM" : a_mn ? "MN" : "K ", (double)h[0] / reps, (double)h[1] / reps,
              cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
