@@ -13,11 +13,14 @@ import sys
 STAGES = {  # bench stage -> kernel name prefixes (one launch each per step)
     "fwd_attention": ["tc5_fwd_kernel"],
     "bwd_dq": ["tc5_dqf_kernel"],
-    "bwd_kv_coarse_tc5": ["tc5_rows2_kernel<0>", "tc5_rows2_kernel<1>", "rows_reduce_kernel"],
+    # levels 1 and 2 both run the hi + lo variant since round 2: two launches
+    "bwd_kv_coarse_tc5": ["tc5_rows2_kernel<1>", "tc5_rows2_kernel<1>#2", "rows_reduce_kernel"],
     "compress": ["pyr12_kernel"],
     "bwd_kv_coarse": ["tc_kv_kernel<2>", "reduce_parts_kernel"],
     "bwd_kv_fine": ["tc5_kvf_kernel"],
-    "select": ["select_coarsest_kernel", "select_level_fast_kernel<8>"],
+    "select": ["select_coarsest_kernel", "select_level_rb_kernel<128>"],
+    "transpose": ["count_all_kernel", "scan_all_kernel", "scatter_all_kernel",
+                  "segment_order_all_kernel"],
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -35,7 +38,10 @@ def kernels(rep):
         b = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             b += float(r[c[m]].replace(",", "")) * SCALE.get(units[c[m]], 1)
-        out.setdefault(name, b)  # first capture of each kernel
+        # first capture of each launch in order; the second launch of the same
+        # kernel within a step is "<name>#2"
+        key = name if name not in out else f"{name}#2"
+        out.setdefault(key, b)
     return out
 
 
