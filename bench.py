@@ -623,7 +623,8 @@ def main() -> None:
         try:
             dense = dense_sdpa(n, units, dev)
             fwd_only = sum(t_ for s_, t_ in stages
-                           if s_ in ("compress", "select", "fwd_prep", "fwd_attention"))
+                           if s_ in ("compress", "select", "compress+select", "fwd_prep",
+                                     "fwd_attention"))
             dense["llsa_fwd_ms"] = fwd_only
             dense["speedup_fwd"] = dense["fwd_ms"] / fwd_only if fwd_only else None
             dense["speedup_fwd_bwd"] = dense["fwd_bwd_ms"] / ms
