@@ -64,6 +64,7 @@ struct TcParams {
   const float *rm_in, *rd_in;        // saved statistics (backward)
   float *lse2, *drow;                // [units][n] backward scratch
   float *dq, *dk, *dv;
+  uint32_t grad_bf16;  // dq/dk/dv are bf16 buffers (tc5_dqf + tc5_kvf write them directly)
   float* part;  // coarse dK'/dV' partials
   uint32_t* flag;
   uint64_t n, pyr_rows, table_entries, csc_off_entries, csc_flat_entries;
@@ -2593,6 +2594,23 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           mbar_arrive(bar(DQFREE + tb));
           mbar_arrive(bar(FFREE + tb));
         }
+        if (p.grad_bf16) {  // bf16 dq: one SW128 [32 rows][64] box per warp
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 8 * k + 2 * e;
+              w[e] = pack_bf16((__uint_as_float(r0[c]) + __uint_as_float(f[c])) * p.scale,
+                               (__uint_as_float(r0[c + 1]) + __uint_as_float(f[c + 1])) * p.scale);
+            }
+            const uint32_t ch = 4 * hh + k;
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                             stg + row * 128 + ((ch ^ (row & 7)) << 4)),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]));
+          }
+          continue;
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float v0 = (__uint_as_float(r0[4 * k]) + __uint_as_float(f[4 * k])) * p.scale;
@@ -2609,7 +2627,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       if (lane == 0) {
         const int y = (int)((uint64_t)unit * p.n + q0 + 32 * (warp & 3));
         tma_store_2d(&m.o, stg + 32 * (warp & 3) * 128, 0, y);
-        tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
+        if (!p.grad_bf16) tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
         bulk_commit();
         bulk_wait_read();
       }
@@ -3143,9 +3161,16 @@ __global__ void __launch_bounds__(kvf::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.f;
       }
-      float* dst = (is_v ? p.dv : p.dk) + ((uint64_t)unit * p.n + kb * kBS) * kD + dcol;
+      const uint64_t o = ((uint64_t)unit * p.n + kb * kBS) * kD + dcol;
+      if (p.grad_bf16) {
+        bf16* dst = reinterpret_cast<bf16*>(is_v ? p.dv : p.dk) + o;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
+        for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = __float2bfloat16_rn(acc[j] + add);
+      } else {
+        float* dst = (is_v ? p.dv : p.dk) + o;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dst[(uint64_t)j * kD] = acc[j] + add;
+      }
     };
     const uint64_t G = gridDim.x;
     EpiFacts fa, fb, fc;  // items it, it+1, it+2 (unrolled by three: no register moves)
@@ -3625,6 +3650,10 @@ TcParams make_params(const Geometry& g) {
 
 }  // namespace
 
+// dq, dk, dv written once each, by tc5_dqf_kernel and tc5_kvf_kernel: they
+// can be written as bf16 directly
+bool tc_bf16_grads_ok(const Geometry& g) { return dqf_path(g) && kvf_path(g); }
+
 bool tc_supported(const Geometry& g, llsa_dtype dt) {
   return dt == LLSA_BF16 && g.d == 64 && g.B == 16 && g.safe && g.n % kTileQ == 0 &&
          g.L >= 1 && g.L <= 4 && coarse_entries(g) <= (uint32_t)kMaxCoarse;
@@ -3792,9 +3821,11 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                         const float* pyr_v, const uint32_t* tables,
                         const uint32_t* csc_offsets, const uint32_t* csc_flat, float* dq,
                         float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s,
-                        StageMarker* mk) {
+                        StageMarker* mk, bool grad_bf16) {
   (void)pyr_k;
   (void)pyr_v;
+  if (grad_bf16 && !tc_bf16_grads_ok(g))
+    return fail(LLSA_ERR_UNSUPPORTED, "bf16 gradients need the fused dQ and fine dK/dV kernels");
   TcParams P = make_params(g);
   P.q = static_cast<const bf16*>(q);
   P.k = static_cast<const bf16*>(k);
@@ -3820,6 +3851,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   P.dq = dq;
   P.dk = dk;
   P.dv = dv;
+  P.grad_bf16 = grad_bf16 ? 1u : 0u;
   static std::atomic<uint64_t> attr{0};
   if (!attrs_done(attr)) {
     LLSA_CUDA_TRY(cudaFuncSetAttribute(tc_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3861,7 +3893,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     const uint64_t in_rows = (uint64_t)units * g.n;
     if (llsa_status st = make_tma_map(&maps.q, q, in_rows, kTileQ)) return st;
     if (llsa_status st = make_tma_map(&maps.g, d_out, in_rows, kTileQ)) return st;
-    if (llsa_status st = make_tma_map(&maps.o, P.dq, in_rows, 32, true)) return st;
+    if (llsa_status st = make_tma_map(&maps.o, P.dq, in_rows, 32, !grad_bf16)) return st;
     const uint64_t tiles = (g.n / kTileQ) * units;
     const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
     tc5_dqf_kernel<<<grid, dqf::kThreads, dqf::kSmem, s>>>(P, maps, units);

@@ -863,7 +863,8 @@ static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* 
                                       const void* v, float* out, void* stream);
 static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const void* q,
                                        const void* k, const void* v, const float* out,
-                                       float* dq, float* dk, float* dv, void* stream);
+                                       float* dq, float* dk, float* dv, void* stream,
+                                       bool grad_bf16 = false);
 
 namespace llsa_impl {
 namespace cvt {
@@ -970,6 +971,9 @@ llsa_status llsa_handle_backward_ex(llsa_handle h, const void* d_out, const void
   if (!h->out32 || out_user != h->last_out16)
     return fail(LLSA_ERR_STALE_STATE,
                 "bf16-output backward needs the bf16 output of this handle's latest forward");
+  if (h->tc && tc_bf16_grads_ok(h->g))  // the kernels write bf16 gradients directly
+    return handle_backward_f32(h, d_out, q, k, v, h->out32, static_cast<float*>(dq),
+                               static_cast<float*>(dk), static_cast<float*>(dv), stream, true);
   const size_t elems = (size_t)h->units * h->g.n * h->g.d;
   {
     DeviceGuard dg(h->device);
@@ -1033,7 +1037,8 @@ static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* 
 
 static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const void* q,
                                        const void* k, const void* v, const float* out,
-                                       float* dq, float* dk, float* dv, void* stream) {
+                                       float* dq, float* dk, float* dv, void* stream,
+                                       bool grad_bf16) {
   NONNULL(h);
   DeviceGuard dg(h->device);
   NONNULL(d_out);
@@ -1059,7 +1064,7 @@ static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const v
     if (h->tc)
       st = tc_backward(g, h->units, d_out, out, h->row_max, h->row_denom, q, k, v, h->pyr_k,
                        h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv, h->tcb,
-                       h->bwd_ws, s, mk);
+                       h->bwd_ws, s, mk, grad_bf16);
     else
       st = simt_backward(g, h->units, h->dt, d_out, out, h->row_max, h->row_denom, q, k, v,
                          h->pyr_k, h->pyr_v, h->tables, h->csc_off, h->csc_flat, dq, dk, dv,

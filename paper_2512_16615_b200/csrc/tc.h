@@ -55,6 +55,8 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                         const float* pyr_v, const uint32_t* tables,
                         const uint32_t* csc_offsets, const uint32_t* csc_flat, float* dq,
                         float* dk, float* dv, const TcBuffers& tb, void* ws, cudaStream_t s,
-                        StageMarker* mk = nullptr);
+                        StageMarker* mk = nullptr, bool grad_bf16 = false);
+// grad_bf16 = true (dq, dk, dv point to bf16 buffers) is valid when this holds
+bool tc_bf16_grads_ok(const Geometry& g);
 
 }  // namespace llsa_impl
