@@ -504,3 +504,54 @@ def test_staged_tensor_core_path_equals_handle(n, L):
     dk, dv = llsa.kv_backward(dO, st, q, k, v, pk, pv, tr, vc)
     llsa.sync_status()
     assert torch.equal(dk, grads[1]) and torch.equal(dv, grads[2])
+
+
+# -------------------------------------------- randomized sweep vs the reference
+def _random_configs(count, seed):
+    """Admissible configs drawn like the reference's own constraints
+    (config.cpp:54-125): n = B^(L+1)·m, K <= n / B^L, L_e <= L.  Every third
+    one has the tensor-core shape (d = 64, B = 16, bf16 inputs)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        tc = len(out) % 3 == 2
+        b = 16 if tc else int(rng.choice([2, 4, 8, 16]))
+        L = int(rng.integers(1, 3 if tc else 4))
+        m = int(rng.integers(1, 5))
+        n = b ** (L + 1) * m
+        if n > 16384 or n < 16:
+            continue
+        kmax = n // b ** L
+        k = int(rng.integers(1, min(kmax, 16) + 1))
+        d = 64 if tc else int(rng.choice([8, 16, 33, 64]))
+        le = int(rng.integers(0, L + 1))
+        mode = int(rng.integers(0, 2))
+        out.append(Config(n, d, b, k, L, le, reweight_mode=mode))
+    return out
+
+
+@pytest.mark.parametrize("cfg", _random_configs(24, 2026),
+                         ids=lambda c: f"n{c.n}d{c.d}B{c.block_size}K{c.top_k}L{c.levels}"
+                         f"e{c.enrich_levels}m{c.reweight_mode}")
+def test_random_configs_match_reference(reference, cfg):
+    # the handle (any shape: SIMT kernels in fp32, tensor cores for bf16 at
+    # d = 64, B = 16) against the compiled reference on its own inputs
+    bf = cfg.d == 64 and cfg.block_size == 16
+    q, k, v, dO = unit_inputs(cfg, 0, seed=7, bf16=bf, backend=reference)
+    ref = reference.run(cfg, q, k, v, dO)
+    dt = torch.bfloat16 if bf else torch.float32
+    h = llsa.LLSAHandle(llsa.LLSAConfig(cfg.n, cfg.d, cfg.block_size, cfg.top_k, cfg.levels,
+                                        cfg.enrich_levels, reweight_mode=cfg.reweight_mode),
+                        1, dt)
+    tq, tk, tv, tdo = (T(a, dt)[None] for a in (q, k, v, dO))
+    out = h.forward(tq, tk, tv)
+    dq, dk, dv = h.backward(tdo, tq, tk, tv, out)
+    llsa.sync_status()
+    np.testing.assert_array_equal(U32(h.view("tables"))[0], ref.tables)
+    np.testing.assert_array_equal(U32(h.view("csc_offsets"))[0], ref.csc_offsets)
+    np.testing.assert_array_equal(U32(h.view("csc_flat"))[0], ref.csc_flat)
+    tol = 2e-2 if h.uses_tensor_cores else 1e-3
+    for name, got, want in (("out", out, ref.out), ("dq", dq, ref.dq), ("dk", dk, ref.dk),
+                            ("dv", dv, ref.dv)):
+        e = rel_err(got[0].cpu().numpy(), want)
+        assert e["max_rel"] <= tol and e["fro"] <= tol, (name, e)
