@@ -78,6 +78,13 @@ struct TcParams {
   // Coarse levels >= hilo_level use the bf16 hi + lo split in S and dP;
   // shallower ones (gain B^l small) use hi only.
   uint32_t hilo_level;
+  // Coarse-entry split (coarse sets past the 24-entry TMEM budget of the
+  // tcgen05 forward / dQ kernels run in two passes): this pass covers plan
+  // entries [ce_base, ce_base + nce); fine_mode 1 = no fine blocks in this
+  // pass — the forward's fine warps contribute the previous pass's (O,
+  // row_max, row_denom) as their partition instead, the dQ fine warps only
+  // D and the LSE, and dq is added to (TMA reduce-add) instead of stored.
+  uint32_t ce_base, fine_mode;
   uint32_t dbg;    // LLSA_DBG: timing probes, see probe()
   uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
   // coarse-level partial layout (kv kernels)
@@ -138,6 +145,7 @@ __device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t role, uint3
 __device__ __forceinline__ void coarse_entry(const TcParams& p, const uint32_t* tab,
                                              uint64_t fb0, uint32_t e, uint32_t& lvl,
                                              uint32_t& row) {
+  e += p.ce_base;
   const uint32_t ksel = p.K * (p.lim - 1);
   uint32_t b;
   if (e < ksel) {
@@ -1441,6 +1449,7 @@ constexpr uint32_t kTmemCols = 512;  // S/dP x2 (256) + dQ x2 (128)
 }  // namespace dqp
 
 __device__ __forceinline__ uint32_t entry_level(const TcParams& p, uint32_t e) {
+  e += p.ce_base;
   const uint32_t ksel = p.K * (p.lim - 1);
   return e < ksel ? 1 + e / p.K : p.L;
 }
@@ -2200,6 +2209,40 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       if (lane == 0) trace_ev(p, crole, i, 3);
     }
     if (lane == 0) bulk_wait_all();  // output stores complete before exit
+  } else if (p.fine_mode == 1) {
+    // ------------------------------------------------------------ previous pass
+    // (second pass of a split coarse set) the fine warps' partition is the
+    // first pass's result for their 16 rows: raw O = O·l, max m, sum l
+    const uint32_t fw = warp - kFine0;
+    uint32_t i = 0;
+    for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
+      const uint32_t unit = (uint32_t)(id / tpu);
+      const uint32_t qs = i % kQStages;
+      const uint64_t row0 = (uint64_t)unit * p.n + (id % tpu) * kTileQ + fw * 16;
+      mbar_wait(bar(QFULL + qs), (i / kQStages) & 1);
+      mbar_arrive(bar(QEMPTY + qs));
+      if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
+      // lane: row r = lane >> 1, 8 float4 groups (half = lane & 1)
+      const uint32_t r = lane >> 1, half = lane & 1;
+      const float l = p.row_denom[row0 + r];
+      const float4* src = reinterpret_cast<const float4*>(p.out + (row0 + r) * kD) + half * 8;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float4 v = src[k];
+        v.x *= l;
+        v.y *= l;
+        v.z *= l;
+        v.w *= l;
+        *reinterpret_cast<float4*>(smem + kOffOf + of_off(fw * 16 + r, half * 8 + k)) = v;
+      }
+      if (half == 0) {
+        const float m2 = p.row_max[row0 + r] * kLog2e;
+        fstat[fw * 16 + r] = m2;
+        fstat[kTileQ + fw * 16 + r] = l;
+        fstat[2 * kTileQ + fw * 16 + r] = m2;
+      }
+      mbar_arrive(bar(FDONE));
+    }
   } else {
     // ------------------------------------------------------------ fine warps
     const float c2 = p.scale * kLog2e;
@@ -2626,8 +2669,13 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         const int y = (int)((uint64_t)unit * p.n + q0 + 32 * (warp & 3));
-        tma_store_2d(&m.o, stg + 32 * (warp & 3) * 128, 0, y);
-        if (!p.grad_bf16) tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
+        if (p.fine_mode) {  // a later pass of a split coarse set: dq += this pass
+          tma_reduce_add_2d(&m.o, stg + 32 * (warp & 3) * 128, 0, y);
+          tma_reduce_add_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
+        } else {
+          tma_store_2d(&m.o, stg + 32 * (warp & 3) * 128, 0, y);
+          if (!p.grad_bf16) tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
+        }
         bulk_commit();
         bulk_wait_read();
       }
@@ -2674,7 +2722,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       constexpr uint32_t sQD = (kFS - 1) * 4096;
 #pragma unroll
       for (uint32_t j = 0; j + 1 < (uint32_t)kFS; ++j)
-        if (j < p.K) load_fine(j);
+        if (j < p.K && !p.fine_mode) load_fine(j);
       load_block16_async(sF + sQD, p.q + in_off + (q0 + fw * 16) * kD, bl, lane);
       load_block16_async(sF + sQD + kTile16, p.dout + in_off + (q0 + fw * 16) * kD, bl, lane);
       cp_async_commit();
@@ -2734,8 +2782,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) dq[j][e] = 0.f;
-      for (uint32_t j = 0; j < p.K; ++j) {
-        if (j + kFS - 1 < p.K) load_fine(j + kFS - 1);
+      const uint32_t nfine = p.fine_mode ? 0u : p.K;  // later passes: coarse entries only
+      for (uint32_t j = 0; j < nfine; ++j) {
+        if (j + kFS - 1 < nfine) load_fine(j + kFS - 1);
         cp_async_commit();
         cp_async_wait<kFS - 1>();
         __syncwarp();
@@ -3525,6 +3574,8 @@ unsigned grid_for(uint64_t threads, int block) {
   return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 
+constexpr uint32_t kMaxCoarsePasses = 3;
+
 uint32_t coarse_entries(const Geometry& g) {
   return g.K * (g.enrich_lim() - 1) + (g.Le == g.L ? (uint32_t)g.level_blocks(g.L) : 0u);
 }
@@ -3542,8 +3593,10 @@ bool fwd5_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   const char* f = getenv("LLSA_FWD5");
   const uint32_t nce = coarse_entries(g);
-  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= fw5::kMaxEntries &&
-         g.K <= 32;
+  // coarse sets past the 24-entry TMEM budget run as several passes of at
+  // most 24 entries (TcParams::ce_base / fine_mode)
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 &&
+         nce <= kMaxCoarsePasses * fw5::kMaxEntries && g.K <= 32;
 }
 
 // tcgen05 fine dK/dV (key-major, gathered queries as M)
@@ -3559,8 +3612,8 @@ bool dqf_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   const char* f = getenv("LLSA_DQF");
   const uint32_t nce = coarse_entries(g);
-  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 && nce <= dqf::kMaxEntries &&
-         g.K <= 32;
+  return !(e && e[0] == '1') && !(f && f[0] == '0') && nce >= 1 &&
+         nce <= kMaxCoarsePasses * dqf::kMaxEntries && g.K <= 32;
 }
 
 void rows_layout(const Geometry& g, TcParams& P) {
@@ -3652,7 +3705,9 @@ TcParams make_params(const Geometry& g) {
 
 // dq, dk, dv written once each, by tc5_dqf_kernel and tc5_kvf_kernel: they
 // can be written as bf16 directly
-bool tc_bf16_grads_ok(const Geometry& g) { return dqf_path(g) && kvf_path(g); }
+bool tc_bf16_grads_ok(const Geometry& g) {
+  return dqf_path(g) && kvf_path(g) && coarse_entries(g) <= dqf::kMaxEntries;  // one dq pass
+}
 
 bool tc_supported(const Geometry& g, llsa_dtype dt) {
   return dt == LLSA_BF16 && g.d == 64 && g.B == 16 && g.safe && g.n % kTileQ == 0 &&
@@ -3794,9 +3849,17 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
     if (llsa_status st = make_tma_map(&maps.o, out, in_rows, 32, true)) return st;
     const uint64_t tiles = (g.n / kTileQ) * units;
     const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
-    tc5_fwd_kernel<<<grid, fw5::kThreads, fw5::kSmem, s>>>(P, maps, units);
-    count_launch();
-    LLSA_LAUNCH_CHECK("tc5_fwd_kernel");
+    // one pass per 24 coarse entries; later passes merge into the output
+    const uint32_t tot = P.nce;
+    for (uint32_t base = 0; base < tot; base += fw5::kMaxEntries) {
+      TcParams Pp = P;
+      Pp.ce_base = base;
+      Pp.nce = tot - base < fw5::kMaxEntries ? tot - base : fw5::kMaxEntries;
+      Pp.fine_mode = base ? 1u : 0u;
+      tc5_fwd_kernel<<<grid, fw5::kThreads, fw5::kSmem, s>>>(Pp, maps, units);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc5_fwd_kernel");
+    }
   } else {
     tc_fwd_kernel<<<dim3((unsigned)(g.n / kTileQ), units), 256, kFwdSmem, s>>>(P);
     count_launch();
@@ -3896,9 +3959,17 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     if (llsa_status st = make_tma_map(&maps.o, P.dq, in_rows, 32, !grad_bf16)) return st;
     const uint64_t tiles = (g.n / kTileQ) * units;
     const unsigned grid = (unsigned)(tiles < (uint64_t)num_sms() ? tiles : num_sms());
-    tc5_dqf_kernel<<<grid, dqf::kThreads, dqf::kSmem, s>>>(P, maps, units);
-    count_launch();
-    LLSA_LAUNCH_CHECK("tc5_dqf_kernel");
+    // one pass per 24 coarse entries; later passes add their dq (TMA reduce)
+    const uint32_t tot = P.nce;
+    for (uint32_t base = 0; base < tot; base += dqf::kMaxEntries) {
+      TcParams Pp = P;
+      Pp.ce_base = base;
+      Pp.nce = tot - base < dqf::kMaxEntries ? tot - base : dqf::kMaxEntries;
+      Pp.fine_mode = base ? 1u : 0u;
+      tc5_dqf_kernel<<<grid, dqf::kThreads, dqf::kSmem, s>>>(Pp, maps, units);
+      count_launch();
+      LLSA_LAUNCH_CHECK("tc5_dqf_kernel");
+    }
     LLSA_MARK(mk, "bwd_dq", s);
   }
   // dq: fine part (+ D, lse2) on mma.sync; coarse part on tcgen05 when enabled

@@ -161,6 +161,14 @@ __device__ __forceinline__ void tma_store_2d(const void* map, uint32_t src, int 
                "r"(x), "r"(y), "r"(src)
                : "memory");
 }
+// element-wise global += tile (fp32 maps): the store form of a TMA reduction
+__device__ __forceinline__ void tma_reduce_add_2d(const void* map, uint32_t src, int x, int y) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], "
+      "[%3];\n" ::"l"(map),
+      "r"(x), "r"(y), "r"(src)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
