@@ -105,6 +105,9 @@ struct TcParams {
   uint64_t rl_qs[kMaxLevels + 2];         // queries per slice
   uint64_t rl_tasks[kMaxLevels + 3];      // task prefix (per unit)
   uint64_t rl_part_off[kMaxLevels + 2];   // float offset per unit
+  uint32_t rl_groups[kMaxLevels + 2];     // 8-block key groups per row
+  uint32_t rl_top[kMaxLevels + 2];        // 1: the coarsest level (one row = all n queries,
+                                          //    its blocks 0 .. n/B^(L+1)-1, no table)
   uint64_t rpart_unit_stride;
 };
 
@@ -1164,12 +1167,18 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   if (li >= p.rl_count) return;
   const uint32_t level = p.rl_level[li];
   const uint64_t b = w - base_w;
-  const uint32_t slices = p.rl_slices[li];
-  const uint32_t* off = p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[level];
+  const uint32_t slices = p.rl_slices[li], groups = p.rl_groups[li];
+  // the coarsest level (rl_top) is one row that holds every block at its
+  // own position; the selected levels find their rows through the CSC
+  const bool top = p.rl_top[li] != 0;
+  const uint32_t* off =
+      top ? nullptr : p.csc_off + (uint64_t)unit * p.csc_off_entries + p.csc_off_off[level];
   const uint32_t* seg =
-      p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[level] + off[b];
-  const uint32_t len = off[b + 1] - off[b];
-  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries + p.table_off[level];
+      top ? nullptr
+          : p.csc_flat + (uint64_t)unit * p.csc_flat_entries + p.csc_flat_off[level] + off[b];
+  const uint32_t len = top ? 1u : off[b + 1] - off[b];
+  const uint32_t* tab = p.tables + (uint64_t)unit * p.table_entries +
+                        (top ? 0 : p.table_off[level]);
   const float* part = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li];
   // thread = (token, 4 d columns) with the token fastest: the partials are
   // [d][key], so 16 neighbouring lanes read 64 contiguous bytes per column
@@ -1182,10 +1191,13 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
   for (uint32_t base = 0; base < len; base += 256) {
     const uint32_t nrow = min(256u, len - base);
     if (threadIdx.x < nrow) {
-      const uint32_t r = seg[base + threadIdx.x];
-      uint32_t pos = 0;
-      for (uint32_t j = 0; j < p.K; ++j)
-        if (tab[(uint64_t)r * p.K + j] == b) pos = j;
+      uint32_t r = 0, pos = (uint32_t)b;
+      if (!top) {
+        r = seg[base + threadIdx.x];
+        pos = 0;
+        for (uint32_t j = 0; j < p.K; ++j)
+          if (tab[(uint64_t)r * p.K + j] == b) pos = j;
+      }
       s_row[threadIdx.x] = r;
       s_pos[threadIdx.x] = pos;
     }
@@ -1193,11 +1205,11 @@ __global__ void __launch_bounds__(256) rows_reduce_kernel(TcParams p, uint32_t u
     for (uint32_t si = 0; si < nrow; ++si) {
       const uint32_t r = s_row[si], pos = s_pos[si];
       const uint32_t g = pos / 8, key = (pos % 8) * kBS + tok;
-      const float* src0 = part + ((uint64_t)r * slices * p.groups + g) * (2 * rows::kKeys * kD) +
+      const float* src0 = part + ((uint64_t)r * slices * groups + g) * (2 * rows::kKeys * kD) +
                           (uint64_t)c4 * rows::kKeys + key;
 #pragma unroll 4
       for (uint32_t s = 0; s < slices; ++s) {
-        const float* src = src0 + (uint64_t)s * p.groups * (2 * rows::kKeys * kD);
+        const float* src = src0 + (uint64_t)s * groups * (2 * rows::kKeys * kD);
         const float* srv = src + rows::kKeys * kD;
         const float4 x = make_float4(__ldg(src), __ldg(src + rows::kKeys),
                                      __ldg(src + 2 * rows::kKeys), __ldg(src + 3 * rows::kKeys));
@@ -3293,7 +3305,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
   const uint64_t tpu = p.rl_tasks[li + 1] - p.rl_tasks[li];
   const uint64_t total = tpu * units;
   const uint32_t level = p.rl_level[li], slices = p.rl_slices[li];
-  const uint64_t span = p.pow[level + 1], qs = p.rl_qs[li];
+  const bool top = p.rl_top[li] != 0;
+  const uint32_t groups = p.rl_groups[li];
+  const uint64_t span = top ? p.n : p.pow[level + 1], qs = p.rl_qs[li];
   const uint32_t ntiles = (uint32_t)(qs / kQT);
   const uint64_t G = gridDim.x;
   // item → (unit, row, slice, group)
@@ -3301,8 +3315,8 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
                     uint32_t& group) {
     unit = (uint32_t)(id / tpu);
     const uint64_t task = id % tpu;
-    group = (uint32_t)(task % p.groups);
-    const uint64_t rs = task / p.groups;
+    group = (uint32_t)(task % groups);
+    const uint64_t rs = task / groups;
     slice = (uint32_t)(rs % slices);
     row = rs / slices;
   };
@@ -3365,6 +3379,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       decode(id, unit, row, slice, group);
       // K not a multiple of 8: the last group's tail lanes gather block 0 as
       // dummy keys; their dK'/dV' rows are never read by rows_reduce_kernel
+      if (top) return group * 8 + lane < nblk ? group * 8 + lane : 0u;
       if (group * 8 + lane >= p.K) return 0u;
       return p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K +
                       group * 8 + lane];
@@ -3524,7 +3539,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       fence_after();
       // transposed partial [64 d][128 keys] (dK', then dV'): for one d a
       // warp's 32 keys are one coalesced 128-byte store
-      const uint64_t pidx = (row * slices + slice) * p.groups + group;
+      const uint64_t pidx = (row * slices + slice) * groups + group;
       float* dst = p.rpart + (uint64_t)unit * p.rpart_unit_stride + p.rl_part_off[li] +
                    pidx * (2 * kKeys * kD) + krow;
 #pragma unroll
@@ -3616,25 +3631,43 @@ bool dqf_path(const Geometry& g) {
          nce <= kMaxCoarsePasses * dqf::kMaxEntries && g.K <= 32;
 }
 
+// Whether the coarsest level (L_e = L: every query attends its n/B^(L+1)
+// blocks) also runs on the tcgen05 row kernel, as one row of all n queries
+// whose key groups are the level's blocks (dummy-padded to 8).
+// With fewer than 4 coarsest blocks (C3: one) the 128-key groups would be
+// mostly dummy keys and the key-major tc_kv kernel is faster (measured: C3
+// 0.465 → 0.551 ms for the coarse stages; C2, C5 with four blocks gain).
+bool rows_top(const Geometry& g) {
+  const char* r2 = getenv("LLSA_ROWS2");
+  const char* t = getenv("LLSA_ROWS_TOP");
+  return rows_path(g) && g.Le == g.L && g.level_blocks(g.L) >= 4 && !(r2 && r2[0] == '0') &&
+         !(t && t[0] == '0');
+}
+
 void rows_layout(const Geometry& g, TcParams& P) {
   P.rows_on = rows_path(g) ? 1u : 0u;
   P.rl_count = 0;
   P.groups = (g.K + 7) / 8;  // a last partial group carries dummy keys (block 0)
   uint64_t tasks = 0, off = 0;
+  auto add = [&](uint32_t l, uint64_t span, uint64_t rows, uint32_t groups, bool top) {
+    const uint32_t i = P.rl_count++;
+    const uint64_t qs = span < 1024 ? span : 1024;
+    P.rl_level[i] = l;
+    P.rl_qs[i] = qs;
+    P.rl_slices[i] = (uint32_t)(span / qs);
+    P.rl_groups[i] = groups;
+    P.rl_top[i] = top ? 1u : 0u;
+    P.rl_tasks[i] = tasks;
+    const uint64_t parts = rows * P.rl_slices[i] * groups;
+    tasks += parts;
+    P.rl_part_off[i] = off;
+    off += parts * 2 * rows::kKeys * kD;
+  };
   if (P.rows_on) {
-    for (uint32_t l = 1; l < g.enrich_lim(); ++l) {
-      const uint32_t i = P.rl_count++;
-      const uint64_t span = g.pow[l + 1];
-      const uint64_t qs = span < 1024 ? span : 1024;
-      P.rl_level[i] = l;
-      P.rl_qs[i] = qs;
-      P.rl_slices[i] = (uint32_t)(span / qs);
-      P.rl_tasks[i] = tasks;
-      const uint64_t parts = g.level_blocks(l) * P.rl_slices[i] * P.groups;
-      tasks += parts;
-      P.rl_part_off[i] = off;
-      off += parts * 2 * rows::kKeys * kD;
-    }
+    for (uint32_t l = 1; l < g.enrich_lim(); ++l)
+      add(l, g.pow[l + 1], g.level_blocks(l), P.groups, false);
+    if (rows_top(g))
+      add(g.L, g.n, 1, (uint32_t)((g.level_blocks(g.L) + 7) / 8), true);
   }
   P.rl_tasks[P.rl_count] = tasks;
   P.rpart_unit_stride = off;
@@ -3648,7 +3681,7 @@ void coarse_slots(const Geometry& g, TcParams& P) {
     const uint32_t i = P.ncl++;
     uint64_t s = avg_queries / 2048;
     s = s < 1 ? 1 : s > 256 ? 256 : s;
-    if (rows && l < g.enrich_lim()) s = 1;  // reduced by rows_reduce_kernel
+    if (rows && (l < g.enrich_lim() || rows_top(g))) s = 1;  // reduced by rows_reduce_kernel
     P.cl_level[i] = l;
     P.cl_split[i] = (uint32_t)s;
     P.cl_tasks[i] = tasks;
