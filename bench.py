@@ -494,8 +494,18 @@ def main() -> None:
 
     import paper_2512_16615_b200 as llsa
 
+    # LLSA_BENCH_SHARE_GPU=1: ranks share the visible GPUs round-robin and
+    # talk over gloo (a multi-rank dry run of this launch path on a box with
+    # fewer GPUs than ranks; NCCL needs one GPU per rank).  The data path has
+    # no collective either way.
+    share = os.environ.get("LLSA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     units = args.units
