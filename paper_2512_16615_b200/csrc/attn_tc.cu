@@ -99,6 +99,7 @@ struct TcParams {
   // (level, selection row, query slice, 8-block key group)
   float* rpart;                           // row partials
   uint32_t rows_on, groups;               // path enabled; key groups per row (ceil(K/8))
+  uint32_t rows_atomic;                   // rows2 reduces into the level slots (TMA add)
   uint32_t rl_count;                      // levels handled (1..lim-1)
   uint32_t rl_level[kMaxLevels + 2];
   uint32_t rl_slices[kMaxLevels + 2];     // query slices per row
@@ -3281,7 +3282,11 @@ struct L {
   static constexpr int kKeyBuf = (LO ? 3 : 2) * kArr;  // Khi, Vhi (, Klo)
   static constexpr int kOffQ = kKeyBufs * kKeyBuf;
   static constexpr int kOffP = kOffQ + kQRing * kQStage;  // P^T, dS^T x 2
-  static constexpr int kOffBar = kOffP + 2 * 2 * 16384;
+  // reduce-add staging per epilogue warp: kStgBufs x (2 blocks x one 16-row,
+  // 32-column fp32 SW128 box of 2 KB)
+  static constexpr int kStgBufs = LO ? 2 : 1;
+  static constexpr int kOffStg = kOffP + 2 * 2 * 16384;
+  static constexpr int kOffBar = kOffStg + 4 * kStgBufs * 4096;
   static constexpr int kSmem = kOffBar + 256;
 };
 enum { KFULL = 0, KEMPTY = 2, QFULL = 4, QEMPTY = 8, SREADY = 12, SFREE = 14, PREADY = 16,
@@ -3525,6 +3530,78 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       fence_proxy_async();
       mbar_arrive(bar(PREADY + b));
     }
+  } else if ((warp == 3 || warp >= 12) && p.rows_atomic) {
+    // ------------------------------------------------------------ epilogue warps
+    // (reduce form) each warp's 32 keys = two 16-key blocks of the group:
+    // scaled by the level's pooling coefficients, staged as SW128 fp32 boxes
+    // and added into the level slot by TMA reductions (L2-resident; no raw
+    // partials, no rows_reduce_kernel).  Summation order across rows is
+    // unordered: LLSA_DETERMINISTIC=1 selects the partial + ordered-sum form.
+    const uint32_t qd = warp & 3;
+    const uint32_t lane_off = (32u * qd) << 16;
+    const uint32_t rr = lane & 15, bb = lane >> 4;
+    const uint32_t stg = sbase + Lay::kOffStg + qd * Lay::kStgBufs * 4096;
+    uint32_t sl = 0;
+    while (sl < p.ncl && p.cl_level[sl] != level) ++sl;
+    const float ck = p.cl_ck[sl], cv = p.cl_cv[sl];
+    const uint64_t tok_l = p.n / p.pow[level];
+    const uint64_t nblk = p.n / p.pow[level + 1];
+    uint32_t it = 0, nb = 0;  // nb: bulk groups committed by lane 0
+    for (uint64_t id = blockIdx.x; id < total; id += G, ++it) {
+      uint32_t unit, slice, group;
+      uint64_t row;
+      decode(id, unit, row, slice, group);
+      // this warp's two block ids (lanes 0, 1); ~0u: dummy keys, not added
+      uint32_t blk = ~0u;
+      if (lane < 2) {
+        const uint32_t j = group * 8 + 2 * qd + lane;
+        if (top)
+          blk = j < nblk ? j : ~0u;
+        else if (j < p.K)
+          blk = p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K + j];
+      }
+      const uint32_t blk0 = __shfl_sync(0xffffffffu, blk, 0),
+                     blk1 = __shfl_sync(0xffffffffu, blk, 1);
+      const uint64_t y0 = ((uint64_t)unit * p.part_unit_stride + p.cl_part_off[sl]) / kD;
+      const uint32_t ab = it & 1;
+      mbar_wait(bar(AREADY + ab), (it >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {  // dK' cols 0-31, 32-63, then dV' (+64 in TMEM)
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + 256 + 128 * ab + 32 * q4, r);
+        tmem_ld_wait();
+        if (q4 == 3) {
+          fence_before();
+          mbar_arrive(bar(AFREE + ab));
+        }
+        // the staging buffer's previous reduction must have read it
+        if (lane == 0 && nb >= (uint32_t)Lay::kStgBufs) bulk_wait_read_n<Lay::kStgBufs - 1>();
+        __syncwarp();
+        const uint32_t buf = stg + (q4 % Lay::kStgBufs) * 4096 + bb * 2048 + rr * 128;
+        const float c = q4 < 2 ? ck : cv;
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4)
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(
+                           buf + ((c4 ^ (rr & 7)) << 4)),
+                       "f"(__uint_as_float(r[4 * c4]) * c), "f"(__uint_as_float(r[4 * c4 + 1]) * c),
+                       "f"(__uint_as_float(r[4 * c4 + 2]) * c),
+                       "f"(__uint_as_float(r[4 * c4 + 3]) * c));
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t src = stg + (q4 % Lay::kStgBufs) * 4096;
+          const uint64_t yb = y0 + (q4 >= 2 ? (uint64_t)p.cl_split[sl] * tok_l : 0);
+          const int x = 32 * (q4 & 1);
+          if (blk0 != ~0u) tma_reduce_add_2d(&m.o, src, x, (int)(yb + (uint64_t)blk0 * kBS));
+          if (blk1 != ~0u)
+            tma_reduce_add_2d(&m.o, src + 2048, x, (int)(yb + (uint64_t)blk1 * kBS));
+          bulk_commit();
+          ++nb;
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();
   } else if (warp == 3 || warp >= 12) {
     // ------------------------------------------------------------ epilogue warps
     const uint32_t krow = 32 * (warp & 3) + lane;
@@ -3731,6 +3808,11 @@ TcParams make_params(const Geometry& g) {
   P.hilo_level = hl ? (uint32_t)atoi(hl) : 1u;
   coarse_slots(g, P);
   rows_layout(g, P);
+  // rows2 adds its items into the level slots with TMA reductions (fp32,
+  // unordered); LLSA_DETERMINISTIC=1 keeps the raw partials and sums them in
+  // a fixed order (rows_reduce_kernel): bitwise run-to-run reproducible
+  const char* det = getenv("LLSA_DETERMINISTIC");
+  P.rows_atomic = P.rows_on && !(det && det[0] == '1') ? 1u : 0u;
   return P;
 }
 
@@ -4044,10 +4126,20 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
     const char* r2 = getenv("LLSA_ROWS2");
     const bool persistent = !(r2 && r2[0] == '0');
     TmaMaps qmaps{};
+    if (!persistent) P.rows_atomic = 0;
     if (persistent) {
       const uint64_t in_rows = (uint64_t)units * g.n;
       if (llsa_status st = make_tma_map(&qmaps.q, q, in_rows, rows2::kQT)) return st;
       if (llsa_status st = make_tma_map(&qmaps.g, d_out, in_rows, rows2::kQT)) return st;
+    }
+    if (P.rows_atomic) {
+      // the level slots [0, rl_count) (a prefix of every unit's slot area)
+      // start at zero; rows2 adds every item into them
+      if (llsa_status st = make_tma_map(&qmaps.o, P.part, units * P.part_unit_stride / kD, kBS,
+                                        true))
+        return st;
+      const uint64_t width = P.rl_count < P.ncl ? P.cl_part_off[P.rl_count] : P.part_unit_stride;
+      LLSA_CUDA_TRY(cudaMemset2DAsync(P.part, P.part_unit_stride * 4, 0, width * 4, units, s));
     }
     for (uint32_t li = 0; li < P.rl_count; ++li) {
       const uint64_t tasks = (P.rl_tasks[li + 1] - P.rl_tasks[li]) * units;
@@ -4073,11 +4165,13 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       count_launch();
       LLSA_LAUNCH_CHECK("tc5_kv_rows_kernel");
     }
-    uint64_t wpu = 0;
-    for (uint32_t li = 0; li < P.rl_count; ++li) wpu += g.level_blocks(P.rl_level[li]);
-    rows_reduce_kernel<<<(unsigned)(wpu * units), 256, 0, s>>>(P, units, wpu);
-    count_launch();
-    LLSA_LAUNCH_CHECK("rows_reduce_kernel");
+    if (!P.rows_atomic) {
+      uint64_t wpu = 0;
+      for (uint32_t li = 0; li < P.rl_count; ++li) wpu += g.level_blocks(P.rl_level[li]);
+      rows_reduce_kernel<<<(unsigned)(wpu * units), 256, 0, s>>>(P, units, wpu);
+      count_launch();
+      LLSA_LAUNCH_CHECK("rows_reduce_kernel");
+    }
   }
   LLSA_MARK(mk, "bwd_kv_coarse_tc5", s);
   if (start < P.ncl) {

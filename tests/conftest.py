@@ -38,3 +38,11 @@ def golden():
     return {"kats": kats,
             "small": dict(np.load(os.path.join(g, "ref_small.npz"))),
             "tables": dict(np.load(os.path.join(g, "ref_tables.npz")))}
+
+
+@pytest.fixture
+def deterministic(monkeypatch):
+    """Fixed-order coarse dK'/dV' summation (LLSA_DETERMINISTIC=1): the
+    default adds the coarse-row items with unordered fp32 TMA reductions, so
+    bitwise run-to-run / path-to-path equality holds only in this mode."""
+    monkeypatch.setenv("LLSA_DETERMINISTIC", "1")

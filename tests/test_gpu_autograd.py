@@ -32,7 +32,7 @@ def test_full_selection_equals_dense_sdpa():
         assert _rel(a, b) < 2e-2
 
 
-def test_autograd_matches_handle_and_guards_staleness():
+def test_autograd_matches_handle_and_guards_staleness(deterministic):
     n = 4096
     q, k, v, g = (torch.randn(1, 2, n, 64, device="cuda").to(torch.bfloat16) for _ in range(4))
     attn = llsa.LLSAAttention(n)
@@ -52,7 +52,7 @@ def test_autograd_matches_handle_and_guards_staleness():
         y1.backward(g)
 
 
-def test_handle_bf16_outputs_are_rounded_fp32_outputs():
+def test_handle_bf16_outputs_are_rounded_fp32_outputs(deterministic):
     # llsa_handle_forward_ex / backward_ex with bf16 results: exactly the
     # fp32 results rounded to bf16 (RNE); a backward against any other output
     # buffer than the latest forward's raises StaleState

@@ -258,7 +258,7 @@ def _staged(oracle_c, cfg: Config, seed: int, bf: bool):
 @pytest.mark.parametrize("cfg", SMALL, ids=lambda c: f"n{c.n}d{c.d}B{c.block_size}L{c.levels}"
                          f"e{c.enrich_levels}m{c.reweight_mode}s{int(c.safe_softmax)}")
 @pytest.mark.parametrize("bf", [False, True])
-def test_staged_path_matches_oracle(oracle_c, cfg, bf):
+def test_staged_path_matches_oracle(oracle_c, cfg, bf, deterministic):
     # bf16 inputs at d = 64, B = 16 (safe softmax) run the tensor-core kernels
     # behind the staged C ABI (the bf16 bar); everything else the fp32 SIMT
     # kernels (rounding-level agreement)
@@ -330,7 +330,7 @@ def test_zero_cotangent_gives_zero_gradients(oracle_c):
                                     (Config(16384, 64, 16, 8, 2, 2, reweight_mode=1), True),
                                     (Config(16384, 64, 16, 8, 2, 0), True),
                                     (Config(65536, 64, 16, 8, 3, 3), True)])
-def test_handle_path_matches_oracle(oracle_c, reference, cfg, bf):
+def test_handle_path_matches_oracle(oracle_c, reference, cfg, bf, deterministic):
     # the single-threaded C restatement up to C2; the multi-threaded compiled
     # reference at N = 65536 (forward and backward on both units)
     units = 2
@@ -456,7 +456,7 @@ def test_full_size_tensor_core_path_matches_reference(reference, name, cfg):
 # The persistent tcgen05 kernels walk (unit, tile) work items; a multi-unit
 # handle must give every unit exactly what a one-unit handle gives it.
 @pytest.mark.parametrize("n,L", [(16384, 2), (65536, 3)])
-def test_multi_unit_handle_is_per_unit_exact(n, L):
+def test_multi_unit_handle_is_per_unit_exact(n, L, deterministic):
     units = 3
     g = torch.Generator(device="cuda").manual_seed(21)
     q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
@@ -478,7 +478,7 @@ def test_multi_unit_handle_is_per_unit_exact(n, L):
 
 
 @pytest.mark.parametrize("n,L", [(16384, 2), (65536, 3)])
-def test_staged_tensor_core_path_equals_handle(n, L):
+def test_staged_tensor_core_path_equals_handle(n, L, deterministic):
     # the reference-shaped staged C ABI (bf16) runs the handle's kernels:
     # tables, CSC lists, forward and backward bit-identical, 2 units
     units = 2
@@ -555,3 +555,28 @@ def test_random_configs_match_reference(reference, cfg):
                             ("dv", dv, ref.dv)):
         e = rel_err(got[0].cpu().numpy(), want)
         assert e["max_rel"] <= tol and e["fro"] <= tol, (name, e)
+
+
+# The default coarse dK'/dV' path adds every (row, group) item into the level
+# slots with fp32 TMA reductions (unordered); LLSA_DETERMINISTIC=1 writes raw
+# partials and sums them in CSC order.  Same math, different fp32 summation
+# order: dq and the output identical, dk / dv equal to fp32 rounding.
+@pytest.mark.parametrize("n,L,Le", [(16384, 2, 2), (65536, 3, 3), (65536, 2, 2),
+                                    (65536, 3, 1)])
+def test_reduce_add_rows_match_ordered_sum(monkeypatch, n, L, Le):
+    units = 2
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
+                   for _ in range(4))
+    cfg = llsa.LLSAConfig(n, 64, 16, 8, L, Le)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("LLSA_DETERMINISTIC", mode)
+        h = llsa.LLSAHandle(cfg, units)
+        out = h.forward(q, k, v)
+        res[mode] = (out,) + tuple(h.backward(dO, q, k, v, out))
+    llsa.sync_status()
+    a, b = res["0"], res["1"]
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    for x, y in zip(a[2:], b[2:]):
+        assert float((x - y).abs().max()) <= 1e-5 * float(y.abs().max())
