@@ -100,6 +100,7 @@ struct TcParams {
   float* rpart;                           // row partials
   uint32_t rows_on, groups;               // path enabled; key groups per row (ceil(K/8))
   uint32_t rows_atomic;                   // rows2 reduces into the level slots (TMA add)
+  uint32_t kv_atomic;                     // tc_kv coarse splits add into split 0 (red.add)
   uint32_t rl_count;                      // levels handled (1..lim-1)
   uint32_t rl_level[kMaxLevels + 2];
   uint32_t rl_slices[kMaxLevels + 2];     // query slices per row
@@ -863,7 +864,26 @@ __global__ void __launch_bounds__(kKvWarps * 32, KvCfg<(MODE > 0)>::MinBlocks)
   cp_async_wait<0>();
 
   const uint32_t r = lane >> 2;
-  if (COARSE) {
+  if (COARSE && p.kv_atomic) {
+    // scaled partial sums added into split 0 of the slot (zeroed by the host;
+    // unordered fp32 adds: LLSA_DETERMINISTIC=1 keeps the split partials)
+    const uint64_t tok_l = p.n / p.pow[level];
+    float* pk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[slot];
+    float* pv = pk + (uint64_t)nsplit * tok_l * kD;
+    const float ck = p.cl_ck[slot], cv = p.cl_cv[slot];
+    const uint64_t k0 = blk * kBS + r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      atomicAdd(reinterpret_cast<float2*>(pk + k0 * kD + j * 8 + cc),
+                make_float2(dk[j][0] * ck, dk[j][1] * ck));
+      atomicAdd(reinterpret_cast<float2*>(pk + (k0 + 8) * kD + j * 8 + cc),
+                make_float2(dk[j][2] * ck, dk[j][3] * ck));
+      atomicAdd(reinterpret_cast<float2*>(pv + k0 * kD + j * 8 + cc),
+                make_float2(dv[j][0] * cv, dv[j][1] * cv));
+      atomicAdd(reinterpret_cast<float2*>(pv + (k0 + 8) * kD + j * 8 + cc),
+                make_float2(dv[j][2] * cv, dv[j][3] * cv));
+    }
+  } else if (COARSE) {
     // raw partial sums for (slot, split): [split][token][64]
     const uint64_t tok_l = p.n / p.pow[level];
     float* pk = p.part + (uint64_t)unit * p.part_unit_stride + p.cl_part_off[slot] +
@@ -3756,7 +3776,11 @@ void coarse_slots(const Geometry& g, TcParams& P) {
   const bool rows = rows_path(g);
   auto add = [&](uint32_t l, uint64_t avg_queries, uint64_t blocks) {
     const uint32_t i = P.ncl++;
-    uint64_t s = avg_queries / 2048;
+    static const uint64_t qpt = [] {  // queries per split task (dev knob)
+      const char* e = getenv("LLSA_KV_SPLIT_Q");
+      return e ? (uint64_t)atoll(e) : 2048ull;
+    }();
+    uint64_t s = avg_queries / qpt;
     s = s < 1 ? 1 : s > 256 ? 256 : s;
     if (rows && (l < g.enrich_lim() || rows_top(g))) s = 1;  // reduced by rows_reduce_kernel
     P.cl_level[i] = l;
@@ -3812,7 +3836,9 @@ TcParams make_params(const Geometry& g) {
   // unordered); LLSA_DETERMINISTIC=1 keeps the raw partials and sums them in
   // a fixed order (rows_reduce_kernel): bitwise run-to-run reproducible
   const char* det = getenv("LLSA_DETERMINISTIC");
-  P.rows_atomic = P.rows_on && !(det && det[0] == '1') ? 1u : 0u;
+  const bool unordered = !(det && det[0] == '1');
+  P.rows_atomic = P.rows_on && unordered ? 1u : 0u;
+  P.kv_atomic = unordered ? 1u : 0u;
   return P;
 }
 
@@ -4122,6 +4148,10 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   if (dq5) LLSA_MARK(mk, "bwd_dq_coarse_tc5", s);
   // levels 1..lim-1 on tcgen05 (row-major), the rest on the key-major kernel
   const uint32_t start = P.rows_on ? P.rl_count : 0;
+  // unordered mode: every coarse slot starts at zero and both coarse kernels
+  // add into it (rows2 by TMA reductions, tc_kv by red.add), no reduce passes
+  if (P.kv_atomic && P.ncl)
+    LLSA_CUDA_TRY(cudaMemsetAsync(P.part, 0, (size_t)units * P.part_unit_stride * 4, s));
   if (P.rows_on) {
     const char* r2 = getenv("LLSA_ROWS2");
     const bool persistent = !(r2 && r2[0] == '0');
@@ -4132,15 +4162,9 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       if (llsa_status st = make_tma_map(&qmaps.q, q, in_rows, rows2::kQT)) return st;
       if (llsa_status st = make_tma_map(&qmaps.g, d_out, in_rows, rows2::kQT)) return st;
     }
-    if (P.rows_atomic) {
-      // the level slots [0, rl_count) (a prefix of every unit's slot area)
-      // start at zero; rows2 adds every item into them
-      if (llsa_status st = make_tma_map(&qmaps.o, P.part, units * P.part_unit_stride / kD, kBS,
-                                        true))
-        return st;
-      const uint64_t width = P.rl_count < P.ncl ? P.cl_part_off[P.rl_count] : P.part_unit_stride;
-      LLSA_CUDA_TRY(cudaMemset2DAsync(P.part, P.part_unit_stride * 4, 0, width * 4, units, s));
-    }
+    if (P.rows_atomic &&
+        make_tma_map(&qmaps.o, P.part, units * P.part_unit_stride / kD, kBS, true))
+      return LLSA_ERR_CUDA;
     for (uint32_t li = 0; li < P.rl_count; ++li) {
       const uint64_t tasks = (P.rl_tasks[li + 1] - P.rl_tasks[li]) * units;
       const bool lo = P.rl_level[li] >= P.hilo_level;
@@ -4194,10 +4218,12 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       count_launch();
       LLSA_LAUNCH_CHECK("tc_kv_kernel<coarse hi>");
     }
-    reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units, start,
-                                                                            P.ncl);
-    count_launch();
-    LLSA_LAUNCH_CHECK("reduce_parts_kernel");
+    if (!P.kv_atomic) {
+      reduce_parts_kernel<<<grid_for(g.n / 16 * kD * units, 256), 256, 0, s>>>(P, units, start,
+                                                                              P.ncl);
+      count_launch();
+      LLSA_LAUNCH_CHECK("reduce_parts_kernel");
+    }
   }
   LLSA_MARK(mk, "bwd_kv_coarse", s);
   if (kvf_path(g)) {

@@ -20,7 +20,8 @@ lib = llsa._lib.load()
 buf = (C.c_ulonglong * 8192)()
 which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
 if which == "bwd" and len(sys.argv) > 2:
-    os.environ.update({"LLSA_KVF": "0"} if sys.argv[2] == "dq" else {})
+    os.environ.update({"LLSA_KVF": "0"} if sys.argv[2] == "dq" else
+                      {"LLSA_DQF": "0"} if sys.argv[2] == "kv" else {})
 dO = torch.randn_like(q)
 g = [torch.empty(units, n, 64, device="cuda") for _ in range(3)]
 for it in range(2):
