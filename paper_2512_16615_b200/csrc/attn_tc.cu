@@ -2520,6 +2520,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           if (lo) load_block16_async(dst + 8192 + e * 2048, p.klo + o, bl, lane);
         }
         cp_async_mbar_arrive(bar(KFULL + s));
+        if (lane == 0) trace_ev(p, 1, rc, 2);
       }
     }
   } else if (warp == 1) {
@@ -2533,7 +2534,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
           const uint32_t s = c % kCRing, b = c & 1;
           mbar_wait(bar(KFULL + s), (c / kCRing) & 1);
+          trace_ev(p, 3, c, 1);
           if (c >= 2) mbar_wait(bar(TFREE + b), ((c >> 1) - 1) & 1);
+          trace_ev(p, 3, c, 2);
           fence_proxy_async();  // gathered cp.async data → async proxy
           fence_after();
           const uint32_t info = ch_info[ch], ne = info & 0xFF;
@@ -2566,7 +2569,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
           const uint32_t s = c % kCRing, b = c & 1, ne = ch_info[ch] & 0xFF;
           mbar_wait(bar(DSREADY + b), (c >> 1) & 1);
+          trace_ev(p, 6, c, 1);
           if (ch == 0 && i >= 2) mbar_wait(bar(DQFREE + tb), ((i >> 1) - 1) & 1);
+          trace_ev(p, 6, c, 2);
           fence_proxy_async();
           fence_after();
           const uint32_t sds = sbase + kOffDS + b * kDSBytes;
@@ -2588,15 +2593,22 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
     const uint32_t row = 32 * (warp & 3) + lane;
     const uint32_t lane_off = (32u * (warp & 3)) << 16;
     uint32_t c = 0, i = 0;
+    // this warp's dq TMA store of the previous tile may still be reading its
+    // rows of the dS ring: waited for only before the next dS store
+    bool st_pending = false;
     for (uint64_t id = blockIdx.x; id < total; id += gridDim.x, ++i) {
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint64_t q0 = (id % tpu) * kTileQ;
       const uint32_t tb = i & 1;
+      if (tid == 96) trace_ev(p, 7, i, 5);
       mbar_wait(bar(DREADY + tb), (i >> 1) & 1);
+      if (tid == 96) trace_ev(p, 7, i, 6);
       const float lse = stat[tb * 256 + row], Drow = stat[tb * 256 + 128 + row];
       for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
         const uint32_t b = c & 1, ne = ch_info[ch] & 0xFF;
+        if (tid == 96) trace_ev(p, 4, c, 1);
         mbar_wait(bar(SREADY + b), (c >> 1) & 1);
+        if (tid == 96) trace_ev(p, 4, c, 2);
         fence_after();
         const uint32_t sds = sbase + kOffDS + b * kDSBytes;
 #pragma unroll
@@ -2608,6 +2620,11 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
             // the dS slot is needed only from the first store on: wait for
             // it while the TMEM loads are in flight
             if (hh == 0 && c >= 2) mbar_wait(bar(DSFREE + b), ((c >> 1) - 1) & 1);
+            if (hh == 0 && st_pending) {
+              if (lane == 0) bulk_wait_read();
+              __syncwarp();
+              st_pending = false;
+            }
             tmem_ld_wait();
             if (2 * hh + 2 >= (int)ne) {  // S / dP all in registers: release the buffer
               fence_before();
@@ -2700,6 +2717,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       }
       fence_proxy_async();
       __syncwarp();
+      if (tid == 96) trace_ev(p, 7, i, 3);
       if (lane == 0) {
         const int y = (int)((uint64_t)unit * p.n + q0 + 32 * (warp & 3));
         if (p.fine_mode) {  // a later pass of a split coarse set: dq += this pass
@@ -2710,9 +2728,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
           if (!p.grad_bf16) tma_store_2d(&m.o, stg + kDSBytes + 32 * (warp & 3) * 128, 32, y);
         }
         bulk_commit();
-        bulk_wait_read();
       }
+      st_pending = true;
       __syncwarp();
+      if (tid == 96) trace_ev(p, 7, i, 4);
     }
     if (lane == 0) bulk_wait_all();  // dq stores complete before exit
   } else if (warp >= 7) {
@@ -2757,6 +2776,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       for (uint32_t j = 0; j + 1 < (uint32_t)kFS; ++j)
         if (j < p.K && !p.fine_mode) load_fine(j);
       load_block16_async(sF + sQD, p.q + in_off + (q0 + fw * 16) * kD, bl, lane);
+      if (tid == 224) trace_ev(p, 5, i, 4);
       load_block16_async(sF + sQD + kTile16, p.dout + in_off + (q0 + fw * 16) * kD, bl, lane);
       cp_async_commit();
       next_ids = fine_ids(id + gridDim.x);
@@ -2806,6 +2826,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
         stat[tb * 256 + 128 + fw * 16 + rr] = dsum;
       }
       mbar_arrive(bar(DREADY + tb));
+      if (tid == 224) trace_ev(p, 5, i, 3);
       const float D0 = __shfl_sync(0xffffffffu, dsum, 2 * r);
       const float D1 = __shfl_sync(0xffffffffu, dsum, 2 * (r + 8));
       const float lse0 = __shfl_sync(0xffffffffu, lse_r, 2 * r);
