@@ -3482,6 +3482,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
             if (LO) mma_bf16(tS, desc_kmajor(sK + 2 * kArr + ks * kKStepKMajor), bq, idesc_s, 1);
           }
           commit(bar(SREADY + b));
+          // the key tiles are read only by these MMAs: the gather may refill
+          // the buffer while the item's last softmax / accumulate run
+          if (j + 1 == ntiles) commit(bar(KEMPTY + kb));
         }
       }
     }
@@ -3509,10 +3512,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
           }
           commit(bar(QEMPTY + s));
           commit(bar(PFREE + b));
-          if (j + 1 == ntiles) {
-            commit(bar(AREADY + ab));
-            commit(bar(KEMPTY + kb));
-          }
+          if (j + 1 == ntiles) commit(bar(AREADY + ab));
         }
       }
     }
