@@ -3316,22 +3316,23 @@ namespace rows2 {
 constexpr int kKeys = 128, kQT = 64;
 constexpr int kArr = kKeys * 128;                 // one 128-key array: 16 KB
 constexpr int kQStage = 17408;                    // Q 8 KB | dO 8 KB | lse | D, 1 KB aligned
-constexpr int kQRing = 4;
 template <bool LO>
 struct L {
   static constexpr int kKeyBufs = LO ? 1 : 2;
+  static constexpr int kQRing = LO ? 5 : 4;
   static constexpr int kKeyBuf = (LO ? 3 : 2) * kArr;  // Khi, Vhi (, Klo)
   static constexpr int kOffQ = kKeyBufs * kKeyBuf;
   static constexpr int kOffP = kOffQ + kQRing * kQStage;  // P^T, dS^T x 2
   // reduce-add staging per epilogue warp: kStgBufs x (2 blocks x one 16-row,
   // 32-column fp32 SW128 box of 2 KB)
-  static constexpr int kStgBufs = LO ? 2 : 1;
+  static constexpr int kStgBufs = 1;
   static constexpr int kOffStg = kOffP + 2 * 2 * 16384;
   static constexpr int kOffBar = kOffStg + 4 * kStgBufs * 4096;
   static constexpr int kSmem = kOffBar + 256;
+  static_assert(kSmem <= 232448, "rows2 shared memory over the 227 KB opt-in limit");
 };
-enum { KFULL = 0, KEMPTY = 2, QFULL = 4, QEMPTY = 8, SREADY = 12, SFREE = 14, PREADY = 16,
-       PFREE = 18, AREADY = 20, AFREE = 22, NBAR = 24 };
+enum { KFULL = 0, KEMPTY = 2, QFULL = 4, QEMPTY = 9, SREADY = 14, SFREE = 16, PREADY = 18,
+       PFREE = 20, AREADY = 22, AFREE = 24, NBAR = 26 };  // Q ring up to 5 slots
 constexpr int kThreads = 16 * 32;
 constexpr uint32_t kTmemCols = 512;  // S^T|dP^T x 2 at [0, 256), dK'|dV' x 2 at [256, 512)
 }  // namespace rows2
@@ -3378,7 +3379,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       mbar_init(bar(AREADY + i), 1);
       mbar_init(bar(AFREE + i), 128);
     }
-    for (int i = 0; i < kQRing; ++i) {
+    for (int i = 0; i < Lay::kQRing; ++i) {
       mbar_init(bar(QFULL + i), 1);
       mbar_init(bar(QEMPTY + i), 1);
     }
@@ -3402,8 +3403,8 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint64_t q_begin = row * span + (uint64_t)slice * qs;
         const uint64_t ro = (uint64_t)unit * p.n;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
-          const uint32_t s = t % kQRing;
-          if (t >= (uint32_t)kQRing) mbar_wait(bar(QEMPTY + s), ((t / kQRing) - 1) & 1);
+          const uint32_t s = t % Lay::kQRing;
+          if (t >= (uint32_t)Lay::kQRing) mbar_wait(bar(QEMPTY + s), ((t / Lay::kQRing) - 1) & 1);
           const uint32_t dst = sbase + Lay::kOffQ + s * kQStage;
           const uint64_t t0 = q_begin + (uint64_t)j * kQT;
           mbar_expect_tx(bar(QFULL + s), 2 * kQT * 128 + 2 * kQT * 4);
@@ -3465,9 +3466,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint32_t kb = it % Lay::kKeyBufs;
         const uint32_t sK = sbase + kb * Lay::kKeyBuf;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
-          const uint32_t s = t % kQRing, b = t & 1;
+          const uint32_t s = t % Lay::kQRing, b = t & 1;
           if (j == 0) mbar_wait(bar(KFULL + kb), (it / Lay::kKeyBufs) & 1);
-          mbar_wait(bar(QFULL + s), (t / kQRing) & 1);
+          mbar_wait(bar(QFULL + s), (t / Lay::kQRing) & 1);
           if (t >= 2) mbar_wait(bar(SFREE + b), ((t >> 1) - 1) & 1);
           fence_proxy_async();  // gathered key tiles (cp.async) → async proxy
           fence_after();
@@ -3497,7 +3498,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint32_t kb = it % Lay::kKeyBufs, ab = it & 1;
         const uint32_t tDK = tmem + 256 + 128 * ab, tDV = tDK + 64;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
-          const uint32_t s = t % kQRing, b = t & 1;
+          const uint32_t s = t % Lay::kQRing, b = t & 1;
           mbar_wait(bar(PREADY + b), (t >> 1) & 1);
           if (j == 0 && it >= 2) mbar_wait(bar(AFREE + ab), ((it >> 1) - 1) & 1);
           fence_after();
@@ -3524,8 +3525,8 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
     const float c2 = p.scale * kLog2e, bias = p.bias2[level];
     const uint32_t ntot = (uint32_t)((total + G - 1 - blockIdx.x) / G) * ntiles;
     for (uint32_t t = 0; t < ntot; ++t) {
-      const uint32_t s = t % kQRing, b = t & 1;
-      mbar_wait(bar(QFULL + s), (t / kQRing) & 1);
+      const uint32_t s = t % Lay::kQRing, b = t & 1;
+      mbar_wait(bar(QFULL + s), (t / Lay::kQRing) & 1);
       mbar_wait(bar(SREADY + b), (t >> 1) & 1);
       fence_after();
       uint32_t sv[32], pv[32];
