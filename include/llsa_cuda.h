@@ -278,7 +278,10 @@ int llsa_handle_uses_tensor_cores(llsa_handle h);
 llsa_status llsa_handle_forward(llsa_handle h, const void* q, const void* k,
                                 const void* v, float* out, void* stream);
 /* Backward: transpose → backward.  Requires the preceding forward on the
- * same handle and the same q/k/v/out buffers. */
+ * same handle and the same q/k/v/out buffers.  On the tensor-core path the
+ * coarse-level dK'/dV' sums are unordered fp32 reductions by default (dk, dv
+ * reproducible to fp32 rounding); LLSA_DETERMINISTIC=1 in the environment
+ * selects the ordered form (bitwise reproducible, as the reference). */
 llsa_status llsa_handle_backward(llsa_handle h, const void* d_out, const void* q,
                                  const void* k, const void* v, const float* out,
                                  float* dq, float* dk, float* dv, void* stream);
