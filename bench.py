@@ -320,7 +320,9 @@ def run_e2e(kind: str, h, inputs, cfg, dev, stream, steps: int, barrier, max_ove
     copies its results (O, dq, dk, dv) D2H.  Steps are software-pipelined over
     three streams with double-buffered device sets, so H2D of step i+1 and D2H
     of step i-1 overlap step i's kernels (PCIe is full duplex) and the steady
-    state is bound by the larger transfer.
+    state is bound by the larger transfer.  Up to 30 pipelined steps are
+    timed (LLSA_E2E_STEPS, bounded by --steps) so the pipeline fill and drain
+    (one transfer + one compute) weigh little in the per-step figure.
       handle_bf16_out  llsa_handle_forward_ex / backward_ex, bf16 results
       handle_f32_out   llsa_handle_forward / backward, fp32 results
       staged_c_abi     the reference-shaped staged entry points (llsa_build_pyramid
@@ -388,7 +390,7 @@ def run_e2e(kind: str, h, inputs, cfg, dev, stream, steps: int, barrier, max_ove
     e2e_steps(2)
     torch.cuda.synchronize()
     llsa.sync_status()
-    n_e2e = max(3, min(steps, 10))
+    n_e2e = max(3, min(steps, int(os.environ.get("LLSA_E2E_STEPS", "30"))))
     barrier()
     torch.cuda.synchronize()
     e0.record(stream)
