@@ -87,6 +87,7 @@ struct TcParams {
   uint32_t ce_base, fine_mode;
   uint32_t dbg;    // LLSA_DBG: timing probes, see probe()
   uint32_t trace;  // 1: record pipeline timestamps of CTA 0 (LLSA_TRACE=1; debugging)
+  uint32_t trace_rows2;  // LLSA_TRACE_ONLY=rows2: trace only the level-1 rows2 launch
   // coarse-level partial layout (kv kernels)
   uint32_t ncl;  // number of coarse level slots
   uint32_t cl_level[kMaxLevels + 2];
@@ -3404,7 +3405,9 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint64_t ro = (uint64_t)unit * p.n;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
           const uint32_t s = t % Lay::kQRing;
+          trace_ev(p, 2, t, 0);
           if (t >= (uint32_t)Lay::kQRing) mbar_wait(bar(QEMPTY + s), ((t / Lay::kQRing) - 1) & 1);
+          trace_ev(p, 2, t, 1);
           const uint32_t dst = sbase + Lay::kOffQ + s * kQStage;
           const uint64_t t0 = q_begin + (uint64_t)j * kQT;
           mbar_expect_tx(bar(QFULL + s), 2 * kQT * 128 + 2 * kQT * 4);
@@ -3443,8 +3446,10 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         ids = 0;
       }
       const uint32_t kb = it % Lay::kKeyBufs;
+      if (lane == 0) trace_ev(p, 1, it, 0);
       if (it >= (uint32_t)Lay::kKeyBufs)
         mbar_wait(bar(KEMPTY + kb), ((it / Lay::kKeyBufs) - 1) & 1);
+      if (lane == 0) trace_ev(p, 1, it, 1);
       const uint32_t unit = (uint32_t)(id / tpu);
       const uint32_t dst = sbase + kb * Lay::kKeyBuf;
       const uint64_t base = (uint64_t)unit * p.pyr_rows + p.pyr_off[level];
@@ -3456,6 +3461,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         if (LO) load_block16_async(dst + 2 * kArr + b * 2048, p.klo + o, bl, lane);
       }
       cp_async_mbar_arrive(bar(KFULL + kb));
+      if (lane == 0) trace_ev(p, 1, it, 2);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ S^T / dP^T issuer
@@ -3467,9 +3473,13 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint32_t sK = sbase + kb * Lay::kKeyBuf;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
           const uint32_t s = t % Lay::kQRing, b = t & 1;
+          trace_ev(p, 3, t, 0);
           if (j == 0) mbar_wait(bar(KFULL + kb), (it / Lay::kKeyBufs) & 1);
+          trace_ev(p, 3, t, 1);
           mbar_wait(bar(QFULL + s), (t / Lay::kQRing) & 1);
+          trace_ev(p, 3, t, 2);
           if (t >= 2) mbar_wait(bar(SFREE + b), ((t >> 1) - 1) & 1);
+          trace_ev(p, 3, t, 3);
           fence_proxy_async();  // gathered key tiles (cp.async) → async proxy
           fence_after();
           const uint32_t sQ = sbase + Lay::kOffQ + s * kQStage, sG = sQ + kQT * 128;
@@ -3483,6 +3493,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
             if (LO) mma_bf16(tS, desc_kmajor(sK + 2 * kArr + ks * kKStepKMajor), bq, idesc_s, 1);
           }
           commit(bar(SREADY + b));
+          trace_ev(p, 3, t, 4);
           // the key tiles are read only by these MMAs: the gather may refill
           // the buffer while the item's last softmax / accumulate run
           if (j + 1 == ntiles) commit(bar(KEMPTY + kb));
@@ -3499,8 +3510,11 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
         const uint32_t tDK = tmem + 256 + 128 * ab, tDV = tDK + 64;
         for (uint32_t j = 0; j < ntiles; ++j, ++t) {
           const uint32_t s = t % Lay::kQRing, b = t & 1;
+          trace_ev(p, 6, t, 0);
           mbar_wait(bar(PREADY + b), (t >> 1) & 1);
+          trace_ev(p, 6, t, 1);
           if (j == 0 && it >= 2) mbar_wait(bar(AFREE + ab), ((it >> 1) - 1) & 1);
+          trace_ev(p, 6, t, 2);
           fence_after();
           const uint32_t sQ = sbase + Lay::kOffQ + s * kQStage, sG = sQ + kQT * 128;
           const uint32_t sPT = sbase + Lay::kOffP + b * 32768, sDST = sPT + 16384;
@@ -3513,6 +3527,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
           }
           commit(bar(QEMPTY + s));
           commit(bar(PFREE + b));
+          trace_ev(p, 6, t, 3);
           if (j + 1 == ntiles) commit(bar(AREADY + ab));
         }
       }
@@ -3526,8 +3541,10 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
     const uint32_t ntot = (uint32_t)((total + G - 1 - blockIdx.x) / G) * ntiles;
     for (uint32_t t = 0; t < ntot; ++t) {
       const uint32_t s = t % Lay::kQRing, b = t & 1;
+      if (tid == 128) trace_ev(p, 4, t, 0);
       mbar_wait(bar(QFULL + s), (t / Lay::kQRing) & 1);
       mbar_wait(bar(SREADY + b), (t >> 1) & 1);
+      if (tid == 128) trace_ev(p, 4, t, 1);
       fence_after();
       uint32_t sv[32], pv[32];
       tmem_ld32(tmem + lane_off + 128 * b + 32 * qh, sv);
@@ -3535,6 +3552,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       // the P^T / dS^T slot is needed only for the stores: wait for it while
       // the TMEM loads are in flight
       if (t >= 2) mbar_wait(bar(PFREE + b), ((t >> 1) - 1) & 1);
+      if (tid == 128) trace_ev(p, 4, t, 2);
       tmem_ld_wait();
       fence_before();
       mbar_arrive(bar(SFREE + b));
@@ -3571,6 +3589,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
       }
       fence_proxy_async();
       mbar_arrive(bar(PREADY + b));
+      if (tid == 128) trace_ev(p, 4, t, 3);
     }
   } else if ((warp == 3 || warp >= 12) && p.rows_atomic) {
     // ------------------------------------------------------------ epilogue warps
@@ -3717,6 +3736,13 @@ uint32_t coarse_entries(const Geometry& g) {
 // Coarse kv slots: levels 1..lim-1, then the coarsest when L_e = L.
 // The tcgen05 row-major coarse dK/dV kernel handles levels 1..lim-1 when the
 // selection width is a multiple of 8 blocks (one 128-key group = M).
+// dev: LLSA_TRACE_ONLY=rows2 records the trace events of the level-1
+// tc5_rows2 launch only (the other kernels run untraced)
+bool trace_only_rows2() {
+  const char* e = getenv("LLSA_TRACE_ONLY");
+  return e && strcmp(e, "rows2") == 0;
+}
+
 bool rows_path(const Geometry& g) {
   const char* e = getenv("LLSA_NO_TCGEN05");
   return !(e && e[0] == '1') && g.enrich_lim() >= 2;
@@ -3850,6 +3876,11 @@ TcParams make_params(const Geometry& g) {
   P.dbg = dg ? (uint32_t)atoi(dg) : 0u;
   const char* tr = getenv("LLSA_TRACE");
   P.trace = tr && tr[0] == '1' ? 1u : 0u;
+  // (tc_backward gives the rows2 level-1 launch its own flag in that mode)
+  if (trace_only_rows2()) {
+    P.trace_rows2 = P.trace;
+    P.trace = 0;
+  }
   const char* hl = getenv("LLSA_HILO_LEVEL");  // default: hi + lo on every coarse level
   P.hilo_level = hl ? (uint32_t)atoi(hl) : 1u;
   coarse_slots(g, P);
@@ -4192,9 +4223,11 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
       const bool lo = P.rl_level[li] >= P.hilo_level;
       if (persistent) {
         const unsigned grid = (unsigned)(tasks < (uint64_t)num_sms() ? tasks : num_sms());
+        TcParams Pr = P;
+        if (trace_only_rows2()) Pr.trace = P.trace_rows2 && li == 0;
         if (lo)
           tc5_rows2_kernel<true><<<grid, rows2::kThreads, rows2::L<true>::kSmem, s>>>(
-              P, qmaps, li, units);
+              Pr, qmaps, li, units);
         else
           tc5_rows2_kernel<false><<<grid, rows2::kThreads, rows2::L<false>::kSmem, s>>>(
               P, qmaps, li, units);
