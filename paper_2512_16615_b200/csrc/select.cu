@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(256, 4) select_level_fast_kernel(
 // pipe, not shared memory, is the limit.  Same per-pair operations and order
 // as detail::dot (bit-exact scores); same top-K as above.
 template <int NT>
-__global__ void __launch_bounds__(NT) select_level_rb_kernel(
+__global__ void __launch_bounds__(NT, NT == 128 ? 5 : 2) select_level_rb_kernel(
     const float* __restrict__ q, uint64_t q_unit_stride, const float* __restrict__ k,
     uint64_t k_unit_stride, const uint32_t* __restrict__ parent, uint64_t parent_unit_stride,
     uint32_t parent_k, uint32_t key_blocks, uint32_t K, float scale,
@@ -375,9 +375,11 @@ __global__ void __launch_bounds__(NT) select_level_rb_kernel(
   const uint32_t blk = blockIdx.x, unit = blockIdx.y, tid = threadIdx.x;
   const uint32_t C = parent_k * B;
   uint32_t* ids = reinterpret_cast<uint32_t*>(smem);      // 256
-  float* scores = reinterpret_cast<float*>(ids + 256);    // 16 × 256
-  float* sq = scores + 16 * 256;                          // 16 × 64
+  float* sq = reinterpret_cast<float*>(ids + 256);        // 16 × 64
   float* sk = sq + 16 * D;                                // C × LD
+  // the scores (16 × 256) reuse the candidate rows once every dot is done,
+  // so a CTA needs ~39 KB instead of ~55 KB (five CTAs per SM instead of four)
+  float* scores = sk;
   const uint32_t* prow = parent + unit * parent_unit_stride + (uint64_t)blk * parent_k;
   for (uint32_t c = tid; c < C; c += NT) {
     uint32_t pb = prow[c / B];
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(NT) select_level_rb_kernel(
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
+  float sc[B];
   if (tid < C) {
     uint64_t acc[B][2];
 #pragma unroll
@@ -426,8 +429,13 @@ __global__ void __launch_bounds__(NT) select_level_rb_kernel(
       const float s1 = __uint_as_float((uint32_t)(acc[r][0] >> 32));
       const float s2 = __uint_as_float((uint32_t)acc[r][1]);
       const float s3 = __uint_as_float((uint32_t)(acc[r][1] >> 32));
-      scores[r * 256 + tid] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+      sc[r] = __fmul_rn(scale, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
     }
+  }
+  __syncthreads();  // every candidate row has been read: the scores may overwrite them
+  if (tid < C) {
+#pragma unroll
+    for (int r = 0; r < (int)B; ++r) scores[r * 256 + tid] = sc[r];
   }
   __syncthreads();
   topk_rows<NT / 32>(scores, ids, C, K, B, out + unit * out_unit_stride + (uint64_t)blk * B * K,
@@ -470,7 +478,7 @@ llsa_status launch_select_level(const float* q, uint64_t q_unit_stride, const fl
     if (smem <= 200 * 1024) {
       const uint32_t key_blocks = (uint32_t)(k_rows / B);
       if (d == 64) {  // the hot shape: register-blocked scorer
-        const size_t smem_rb = 4 * (256 + 16 * 256 + 16 * 64 + C * 68);
+        const size_t smem_rb = 4 * (256 + 16 * 64 + (C * 68 > 16 * 256 ? C * 68 : 16 * 256));
         auto rb = C <= 128 ? select_level_rb_kernel<128> : select_level_rb_kernel<256>;
         if (smem_rb > 48 * 1024)
           LLSA_CUDA_TRY(cudaFuncSetAttribute(rb, cudaFuncAttributeMaxDynamicSharedMemorySize,
