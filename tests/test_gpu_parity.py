@@ -580,3 +580,29 @@ def test_reduce_add_rows_match_ordered_sum(monkeypatch, n, L, Le):
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     for x, y in zip(a[2:], b[2:]):
         assert float((x - y).abs().max()) <= 1e-5 * float(y.abs().max())
+
+
+# The largest BASELINE batches in one handle — C4's per-GPU batch (128 units
+# of N = 65536) and C5's 16 units of N = 262144: every index, TMA coordinate
+# and work-item decode at full size.  Sampled units must equal a one-unit
+# handle's results bit for bit (ordered mode).
+@pytest.mark.parametrize("units,n", [(128, 65536), (16, 262144)])
+def test_largest_batches_match_single_unit_handle(deterministic, units, n):
+    L = 3
+    g = torch.Generator(device="cuda").manual_seed(44)
+    q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
+                   for _ in range(4))
+    lc = llsa.LLSAConfig(n, 64, 16, 8, L, L)
+    hm = llsa.LLSAHandle(lc, units, torch.bfloat16)
+    out = hm.forward(q, k, v, out_dtype=torch.bfloat16)
+    grads = hm.backward(dO, q, k, v, out)
+    llsa.sync_status()
+    h1 = llsa.LLSAHandle(lc, 1, torch.bfloat16)
+    for u in sorted({0, units // 2 + 5, units - 1}):
+        sl = slice(u, u + 1)
+        o1 = h1.forward(q[sl], k[sl], v[sl], out_dtype=torch.bfloat16)
+        g1 = h1.backward(dO[sl], q[sl], k[sl], v[sl], o1)
+        assert torch.equal(out[sl], o1), u
+        for a, b in zip(grads, g1):
+            assert torch.equal(a[sl], b), u
+    llsa.sync_status()
