@@ -1770,7 +1770,8 @@ __global__ void __launch_bounds__(320, 1)
 // tensor core (P times a ones column).
 struct FineState {
   float o[8][4];
-  float lo[4];           // l in an m16n8 accumulator (column 0 of each row pair)
+  float lo[4];           // l: this lane's partial row sums of rows r, r + 8 in [0], [2]
+                         // (quad-reduced once per tile)
   float m[2], mt[2];     // reference max, true max (log2 units)
 };
 constexpr float kLazy = 8.f;
@@ -1832,9 +1833,12 @@ __device__ __forceinline__ void attend_fine(uint32_t kT, uint32_t vT, float bias
     mma16816(st.o[2 * dn], a, b[0], b[1]);
     mma16816(st.o[2 * dn + 1], a, b[2], b[3]);
   }
-  // row sums of P: B = ones in column n = 0 (lanes with n = lane >> 2 == 0)
-  const uint32_t one = (lane >> 2) == 0 ? 0x3F803F80u : 0u;
-  mma16816(st.lo, a, one, one);
+  // row sums of the bf16-rounded P (what P·V multiplies), per lane in fp32
+  // (FADD instead of a 17th HMMA per block: the fine loop is HMMA-bound)
+  auto lo_f = [](uint32_t x) { return __uint_as_float(x << 16); };
+  auto hi_f = [](uint32_t x) { return __uint_as_float(x & 0xffff0000u); };
+  st.lo[0] += (lo_f(a[0]) + hi_f(a[0])) + (lo_f(a[2]) + hi_f(a[2]));
+  st.lo[2] += (lo_f(a[1]) + hi_f(a[1])) + (lo_f(a[3]) + hi_f(a[3]));
 }
 
 namespace fw5 {
@@ -2349,9 +2353,12 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
       if (i >= 1) mbar_wait(bar(FFREE), (i - 1) & 1);
       if (tid == kFine0 * 32) trace_ev(p, 5, i, 2);
       {
-        // l of rows r, r + 8 sits in column 0 of the l accumulator (lane & 3 == 0)
-        const float lf0 = __shfl_sync(0xffffffffu, st.lo[0], lane & ~3u);
-        const float lf1 = __shfl_sync(0xffffffffu, st.lo[2], lane & ~3u);
+        // l of rows r, r + 8: the quad's partial sums
+        float lf0 = st.lo[0], lf1 = st.lo[2];
+        lf0 += __shfl_xor_sync(0xffffffffu, lf0, 1);
+        lf1 += __shfl_xor_sync(0xffffffffu, lf1, 1);
+        lf0 += __shfl_xor_sync(0xffffffffu, lf0, 2);
+        lf1 += __shfl_xor_sync(0xffffffffu, lf1, 2);
         const uint32_t r0 = fw * 16 + r, r1 = r0 + 8;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
