@@ -42,6 +42,8 @@
 #include "umma.cuh"
 
 namespace llsa_impl {
+static int num_sms();  // SM count of the current device (below)
+
 namespace {
 
 using namespace llsa_tc;
@@ -2419,8 +2421,9 @@ constexpr int kOffEnt = kOffStat + 4 * kTileQ * 4;        // bias[32], chunk inf
 constexpr int kOffBar = kOffEnt + 256;
 enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 7, SREADY = 10, TFREE = 12, DSREADY = 14,
        DSFREE = 16, DQREADY = 18, DQFREE = 20, DREADY = 22, FDONE = 24, FFREE = 26,
-       NBAR = 28 };
+       STATFREE = 28, NBAR = 30 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
+static_assert(kSmem <= 232448, "dqf shared memory over the 227 KB opt-in limit");
 constexpr int kThreads = 16 * 32;
 constexpr uint32_t kTmemCols = 512;  // S/dP x 2 [0, 256), dQ_c x 2 [256, 384), dQ_f x 2 [384, 512)
 constexpr uint32_t kMaxEntries = 24;  // ent_rows[24]
@@ -2467,6 +2470,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       mbar_init(bar(DQREADY + i), 1);
       mbar_init(bar(DQFREE + i), 128);
       mbar_init(bar(DREADY + i), 256);
+      mbar_init(bar(STATFREE + i), 128);  // the coarse warps hold tile i's LSE / D
     }
     fence_mbar_init();
   }
@@ -2612,6 +2616,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       mbar_wait(bar(DREADY + tb), (i >> 1) & 1);
       if (tid == 96) trace_ev(p, 7, i, 6);
       const float lse = stat[tb * 256 + row], Drow = stat[tb * 256 + 128 + row];
+      // the fine warps may overwrite stat[tb] with tile i+2's values only
+      // after this (they can be two tiles ahead of this point: nothing else
+      // orders their tile i+2 start after this read)
+      mbar_arrive(bar(STATFREE + tb));
       for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
         const uint32_t b = c & 1, ne = ch_info[ch] & 0xFF;
         if (tid == 96) trace_ev(p, 4, c, 1);
@@ -2827,6 +2835,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       __syncwarp();  // the Q/dO stage is overwritten by fine block kFS-1
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
       const uint32_t tb = i & 1;
+      if (i >= 2) mbar_wait(bar(STATFREE + tb), ((i >> 1) - 1) & 1);
       if (half == 0) {
         p.drow[ro + trow] = dsum;
         p.lse2[ro + trow] = lse_r;
@@ -3825,10 +3834,19 @@ void rows_layout(const Geometry& g, TcParams& P) {
   P.rpart_unit_stride = off;
 }
 
-void coarse_slots(const Geometry& g, TcParams& P) {
+// units > 0: the launch's batch is known, so a lone key-major coarse slot (C3:
+// the coarsest level's one 16-key block) gets the split count that fills
+// whole waves of 4-warp CTAs, one per SM (C3 × 16: 32 → 37 splits, 0.058 →
+// 0.052 ms; an extra partial wave costs more than the smaller tasks gain).
+// reserve: workspace sizing — the lone slot's layout at the largest split
+// count, so a workspace sized on one device fits a launch on any other.
+void coarse_slots(const Geometry& g, TcParams& P, uint32_t units = 0, bool reserve = false) {
   P.ncl = 0;
   uint64_t tasks = 0, off = 0;
   const bool rows = rows_path(g);
+  uint32_t kv_slots = 0;
+  for (uint32_t l = 1; l < g.enrich_lim(); ++l) kv_slots += rows ? 0u : 1u;
+  if (g.Le == g.L && !(rows && rows_top(g))) ++kv_slots;
   auto add = [&](uint32_t l, uint64_t avg_queries, uint64_t blocks) {
     const uint32_t i = P.ncl++;
     static const uint64_t qpt = [] {  // queries per split task (dev knob)
@@ -3837,7 +3855,22 @@ void coarse_slots(const Geometry& g, TcParams& P) {
     }();
     uint64_t s = avg_queries / qpt;
     s = s < 1 ? 1 : s > 256 ? 256 : s;
-    if (rows && (l < g.enrich_lim() || rows_top(g))) s = 1;  // reduced by rows_reduce_kernel
+    const bool on_rows = rows && (l < g.enrich_lim() || rows_top(g));
+    // (not in the ordered mode, whose per-unit results must not depend on the
+    // batch: the fp32 split sums would change with the split count)
+    const char* det = getenv("LLSA_DETERMINISTIC");
+    const bool ordered = det && det[0] == '1';
+    if (units && kv_slots == 1 && !on_rows && !getenv("LLSA_KV_SPLIT_Q") &&
+        (!ordered || reserve)) {
+      const uint64_t slots = (uint64_t)num_sms() * kKvWarps;  // warps of one wave
+      const uint64_t per = (uint64_t)units * blocks;             // warps per split
+      uint64_t waves = (per * s + slots / 2) / slots;
+      waves = waves < 1 ? 1 : waves;
+      uint64_t fit = waves * slots / per;
+      if (fit >= 1 && fit <= 256) s = fit;
+      if (reserve) s = 256;
+    }
+    if (on_rows) s = 1;  // reduced by rows_reduce_kernel
     P.cl_level[i] = l;
     P.cl_split[i] = (uint32_t)s;
     P.cl_tasks[i] = tasks;
@@ -3855,7 +3888,7 @@ void coarse_slots(const Geometry& g, TcParams& P) {
   P.part_unit_stride = off;
 }
 
-TcParams make_params(const Geometry& g) {
+TcParams make_params(const Geometry& g, uint32_t units) {
   TcParams P{};
   P.n = g.n;
   P.pyr_rows = g.pyr_rows;
@@ -3890,7 +3923,7 @@ TcParams make_params(const Geometry& g) {
   }
   const char* hl = getenv("LLSA_HILO_LEVEL");  // default: hi + lo on every coarse level
   P.hilo_level = hl ? (uint32_t)atoi(hl) : 1u;
-  coarse_slots(g, P);
+  coarse_slots(g, P, units);
   rows_layout(g, P);
   // rows2 adds its items into the level slots with TMA reductions (fp32,
   // unordered); LLSA_DETERMINISTIC=1 keeps the raw partials and sums them in
@@ -4020,7 +4053,7 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
     if (llsa_status st = launch_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
     LLSA_MARK(mk, "fwd_prep", s);
   }
-  TcParams P = make_params(g);
+  TcParams P = make_params(g, units);
   P.q = static_cast<const bf16*>(q);
   P.k = static_cast<const bf16*>(k);
   P.v = static_cast<const bf16*>(v);
@@ -4072,7 +4105,7 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
 
 size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units) {
   TcParams P{};
-  coarse_slots(g, P);
+  coarse_slots(g, P, units, true);
   rows_layout(g, P);
   const size_t rows = ((size_t)units * g.n * 4 + 255) & ~size_t(255);
   const size_t part = ((size_t)units * P.part_unit_stride * 4 + 255) & ~size_t(255);
@@ -4090,7 +4123,7 @@ llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
   (void)pyr_v;
   if (grad_bf16 && !tc_bf16_grads_ok(g))
     return fail(LLSA_ERR_UNSUPPORTED, "bf16 gradients need the fused dQ and fine dK/dV kernels");
-  TcParams P = make_params(g);
+  TcParams P = make_params(g, units);
   P.q = static_cast<const bf16*>(q);
   P.k = static_cast<const bf16*>(k);
   P.v = static_cast<const bf16*>(v);
