@@ -586,13 +586,13 @@ def test_reduce_add_rows_match_ordered_sum(monkeypatch, n, L, Le):
 # of N = 65536) and C5's 16 units of N = 262144: every index, TMA coordinate
 # and work-item decode at full size.  Sampled units must equal a one-unit
 # handle's results bit for bit (ordered mode).
-@pytest.mark.parametrize("units,n", [(128, 65536), (16, 262144)])
-def test_largest_batches_match_single_unit_handle(deterministic, units, n):
-    L = 3
+@pytest.mark.parametrize("units,n,L,K", [(128, 65536, 3, 8), (16, 262144, 3, 8),
+                                         (128, 16384, 2, 8), (16, 262144, 3, 16)])
+def test_largest_batches_match_single_unit_handle(deterministic, units, n, L, K):
     g = torch.Generator(device="cuda").manual_seed(44)
     q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
                    for _ in range(4))
-    lc = llsa.LLSAConfig(n, 64, 16, 8, L, L)
+    lc = llsa.LLSAConfig(n, 64, 16, K, L, L)
     hm = llsa.LLSAHandle(lc, units, torch.bfloat16)
     out = hm.forward(q, k, v, out_dtype=torch.bfloat16)
     grads = hm.backward(dO, q, k, v, out)

@@ -9,11 +9,14 @@ import torch  # noqa: E402
 
 import paper_2512_16615_b200 as llsa  # noqa: E402
 
-units, n, L = int(sys.argv[1]) if len(sys.argv) > 1 else 128, 65536, 3
+a = [int(x) for x in sys.argv[1:]] + [None] * 5
+units, n, L = a[0] or 128, a[1] or 65536, a[2] or 3
+K, Le = a[3] or 8, a[4] if a[4] is not None else L
 g = torch.Generator(device="cuda").manual_seed(44)
 q, k, v, dO = (torch.randn(units, n, 64, device="cuda", generator=g).to(torch.bfloat16)
                for _ in range(4))
-lc = llsa.LLSAConfig(n, 64, 16, 8, L, L)
+lc = llsa.LLSAConfig(n, 64, 16, K, L, Le)
+print(f"units={units} n={n} L={L} K={K} Le={Le}")
 hm = llsa.LLSAHandle(lc, units, torch.bfloat16)
 out = hm.forward(q, k, v, out_dtype=torch.bfloat16)
 gr = hm.backward(dO, q, k, v, out)
