@@ -3636,6 +3636,7 @@ __global__ void __launch_bounds__(rows2::kThreads, 1)
           blk = j < nblk ? j : ~0u;
         else if (j < p.K)
           blk = p.tables[(uint64_t)unit * p.table_entries + p.table_off[level] + row * p.K + j];
+        if (blk >= nblk) blk = ~0u;  // out of range (flagged by the gather warp): not added
       }
       const uint32_t blk0 = __shfl_sync(0xffffffffu, blk, 0),
                      blk1 = __shfl_sync(0xffffffffu, blk, 1);
