@@ -582,6 +582,37 @@ def main() -> None:
     from paper_2512_16615_b200.sharding import max_over_ranks
     ms = max_over_ranks(ms)
 
+    # secondary: the same step with bf16 results (O, dq, dk, dv written as
+    # bf16 by the kernels, llsa_handle_*_ex) — what a bf16 training step and
+    # the e2e line use; the headline keeps the reference's fp32 results
+    ms_bf16 = None
+    if graph is not None:
+        out16, dq16, dk16, dv16 = (torch.empty(shape, device=dev, dtype=torch.bfloat16)
+                                   for _ in range(4))
+
+        def step16():
+            h.forward(q, k, v, out16)
+            h.backward(dO, q, k, v, out16, dq16, dk16, dv16)
+
+        for _ in range(2):
+            step16()
+        g16 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g16):
+            step16()
+        g16.replay()
+        torch.cuda.synchronize()
+        llsa.sync_status()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            g16.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_bf16 = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        llsa.sync_status()
+
     # ---- roofline: every stage, and the dominant one as the headline --------
     peaks, peak_src = _peaks()
     W = algorithmic_work(n, args.levels, units, args.enrich_levels, args.top_k)
@@ -656,6 +687,7 @@ def main() -> None:
                 "stages_ms": {s: round(t_, 4) for s, t_ in stages},
                 "stages_roofline": per_stage,
                 "eager_ms_per_step": eager_ms,
+                "ms_per_step_bf16_outputs": ms_bf16,
                 "timed_launch_mode": "cuda_graph_replay" if graph is not None else "eager",
                 "tensor_cores": h.uses_tensor_cores,
                 "cpu_baseline": cpu, "e2e": e2e, "e2e_variants": e2e_variants, "dense_sdpa": dense, "gpu_launches": launches * args.steps,

@@ -104,6 +104,7 @@ struct TcParams {
   uint32_t rows_on, groups;               // path enabled; key groups per row (ceil(K/8))
   uint32_t rows_atomic;                   // rows2 reduces into the level slots (TMA add)
   uint32_t kv_atomic;                     // tc_kv coarse splits add into split 0 (red.add)
+  void* out16;                            // forward: also write O as bf16 here (or null)
   uint32_t rl_count;                      // levels handled (1..lim-1)
   uint32_t rl_level[kMaxLevels + 2];
   uint32_t rl_slices[kMaxLevels + 2];     // query slices per row
@@ -2229,6 +2230,20 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
         bad |= !isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w);
         *a = v;
       }
+      if (p.out16) {  // bf16 copy (RNE of the fp32 result) of this thread's half
+        // row, re-read from the staging: 32 bf16, 64 contiguous bytes
+        uint4* d = reinterpret_cast<uint4*>(static_cast<bf16*>(p.out16) +
+                                            ((uint64_t)unit * p.n + q0 + row) * kD + 32 * h);
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          const float4 x = *reinterpret_cast<const float4*>(smem + kOffOf +
+                                                            of_off(row, 8 * h + 2 * k));
+          const float4 y = *reinterpret_cast<const float4*>(smem + kOffOf +
+                                                            of_off(row, 8 * h + 2 * k + 1));
+          d[k] = make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y),
+                            pack_bf16(y.z, y.w));
+        }
+      }
       fence_before();
       mbar_arrive(bar(OFREE + ob));
       fence_proxy_async();
@@ -4046,10 +4061,13 @@ llsa_status tc_prep(const Geometry& g, uint32_t units, const float* pyr_k, const
   return launch_prep(g, units, pyr_k, pyr_v, tb, s);
 }
 
+bool tc_forward_writes_bf16(const Geometry& g) { return fwd5_path(g); }
+
 llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const void* k,
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,
-                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk, bool prepped) {
+                       const TcBuffers& tb, cudaStream_t s, StageMarker* mk, bool prepped,
+                       void* out16) {
   if (!prepped) {
     if (llsa_status st = launch_prep(g, units, pyr_k, pyr_v, tb, s)) return st;
     LLSA_MARK(mk, "fwd_prep", s);
@@ -4064,6 +4082,7 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
   P.vlo = tb.v_lo;
   P.tables = tables;
   P.out = out;
+  P.out16 = out16;
   P.row_max = row_max;
   P.row_denom = row_denom;
   static std::atomic<uint64_t> attr{0};
@@ -4091,6 +4110,7 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
       Pp.ce_base = base;
       Pp.nce = tot - base < fw5::kMaxEntries ? tot - base : fw5::kMaxEntries;
       Pp.fine_mode = base ? 1u : 0u;
+      Pp.out16 = base + fw5::kMaxEntries >= tot ? out16 : nullptr;  // the final pass only
       tc5_fwd_kernel<<<grid, fw5::kThreads, fw5::kSmem, s>>>(Pp, maps, units);
       count_launch();
       LLSA_LAUNCH_CHECK("tc5_fwd_kernel");

@@ -860,7 +860,8 @@ int llsa_handle_uses_tensor_cores(llsa_handle h) { return h && h->tc ? 1 : 0; }
 }  // extern "C"
 
 static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* k,
-                                      const void* v, float* out, void* stream);
+                                      const void* v, float* out, void* stream,
+                                      void* out16 = nullptr);
 static llsa_status handle_backward_f32(llsa_handle h, const void* d_out, const void* q,
                                        const void* k, const void* v, const float* out,
                                        float* dq, float* dk, float* dv, void* stream,
@@ -942,13 +943,18 @@ llsa_status llsa_handle_forward_ex(llsa_handle h, const void* q, const void* k, 
     if (llsa_status st = ensure(&h->out32, elems * 4)) return st;
     out = h->out32;
   }
-  llsa_status st = handle_forward_f32(h, q, k, v, out, stream);
+  // the tcgen05 forward writes the bf16 copy in its epilogue; other paths
+  // convert the fp32 output afterwards
+  const bool fused16 = out_dtype == LLSA_BF16 && h->tc && tc_forward_writes_bf16(h->g);
+  llsa_status st = handle_forward_f32(h, q, k, v, out, stream, fused16 ? out_user : nullptr);
   if (!st && out_dtype == LLSA_BF16) {
-    DeviceGuard dg(h->device);
-    const float* src[3] = {h->out32, nullptr, nullptr};
-    void* dst[3] = {out_user, nullptr, nullptr};
-    st = to_bf16(src, dst, 1, elems, S(stream));
-    h->last_launches += 1;
+    if (!fused16) {
+      DeviceGuard dg(h->device);
+      const float* src[3] = {h->out32, nullptr, nullptr};
+      void* dst[3] = {out_user, nullptr, nullptr};
+      st = to_bf16(src, dst, 1, elems, S(stream));
+      h->last_launches += 1;
+    }
     h->last_out16 = out_user;
   }
   return st;
@@ -995,7 +1001,7 @@ llsa_status llsa_handle_backward_ex(llsa_handle h, const void* d_out, const void
 }  // extern "C"
 
 static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* k,
-                                      const void* v, float* out, void* stream) {
+                                      const void* v, float* out, void* stream, void* out16) {
   NONNULL(h);
   DeviceGuard dg(h->device);
   NONNULL(q);
@@ -1024,7 +1030,7 @@ static llsa_status handle_forward_f32(llsa_handle h, const void* q, const void* 
   if (!st) {
     if (h->tc) {
       st = tc_forward(g, h->units, q, k, v, h->pyr_k, h->pyr_v, h->tables, out, h->row_max,
-                      h->row_denom, h->tcb, s, mk, fused);
+                      h->row_denom, h->tcb, s, mk, fused, out16);
     } else {
       st = simt_forward(g, h->units, h->dt, q, k, v, h->pyr_k, h->pyr_v, h->tables, out,
                         h->row_max, h->row_denom, s);

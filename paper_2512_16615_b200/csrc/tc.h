@@ -47,7 +47,10 @@ llsa_status tc_forward(const Geometry& g, uint32_t units, const void* q, const v
                        const void* v, const float* pyr_k, const float* pyr_v,
                        const uint32_t* tables, float* out, float* row_max, float* row_denom,
                        const TcBuffers& tb, cudaStream_t s, StageMarker* mk = nullptr,
-                       bool prepped = false);
+                       bool prepped = false, void* out16 = nullptr);
+// whether tc_forward writes its `out16` (bf16 copy of O) itself (the tcgen05
+// forward); otherwise the caller converts the fp32 output
+bool tc_forward_writes_bf16(const Geometry& g);
 size_t tc_backward_ws_bytes(const Geometry& g, uint32_t units);
 llsa_status tc_backward(const Geometry& g, uint32_t units, const void* d_out,
                         const float* out, const float* row_max, const float* row_denom,
