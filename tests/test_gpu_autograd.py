@@ -74,3 +74,19 @@ def test_handle_bf16_outputs_are_rounded_fp32_outputs(deterministic):
         h.forward(q[:1], k[:1], v[:1])
     with pytest.raises(llsa.ArgumentError):
         h.forward(q.half(), k.half(), v.half())
+
+
+@pytest.mark.parametrize("n,L,K", [(65536, 3, 16), (65536, 3, 8)])
+def test_bf16_outputs_equal_rounded_fp32_on_multi_pass_forward(deterministic, n, L, K):
+    # K = 16 at L = 3: 33 coarse entries run as two tcgen05 forward passes; the
+    # bf16 copy is written by the final pass's epilogue only
+    q, k, v, g = (torch.randn(2, n, 64, device="cuda").to(torch.bfloat16) for _ in range(4))
+    h = llsa.LLSAHandle(llsa.LLSAConfig(n, 64, 16, K, L, L), 2)
+    out32 = h.forward(q, k, v)
+    grads32 = h.backward(g, q, k, v, out32)
+    out16 = h.forward(q, k, v, out_dtype=torch.bfloat16)
+    assert torch.equal(out16, out32.to(torch.bfloat16))
+    grads16 = h.backward(g, q, k, v, out16)
+    for a, b in zip(grads16, grads32):
+        assert torch.equal(a, b.to(torch.bfloat16))
+    llsa.sync_status()
