@@ -2420,7 +2420,7 @@ __global__ void __launch_bounds__(fw5::kThreads, 1)
 //                     (smem for the coarse warps, global for the kv kernels)
 namespace dqf {
 constexpr int kTileBytes = kTileQ * 128;        // 16 KB
-constexpr int kCStage = 4 * 8192;               // Khi, Klo, Vhi, Vlo of 64 keys
+constexpr int kCStage = 3 * 8192;               // Khi, Klo, Vhi of 64 keys (V' hi only)
 constexpr int kCRing = 2;
 constexpr int kQS = 1;                          // Q/dO stages
 constexpr int kDSBytes = kTileQ * 128;          // dS chunk: 128 rows x 64 keys bf16
@@ -2431,12 +2431,15 @@ constexpr int kOffQ = 0;
 constexpr int kOffC = kQS * kQStage;
 constexpr int kOffDS = kOffC + kCRing * kCStage;
 constexpr int kOffFine = kOffDS + 2 * kDSBytes;
-constexpr int kOffStat = kOffFine + 8 * kFineWarp;        // lse, D x 2 tiles
-constexpr int kOffEnt = kOffStat + 4 * kTileQ * 4;        // bias[32], chunk info[8], rows[32]
+// lse, D of three tiles: the fine warps (up to two tiles ahead of the coarse
+// warps' read, bounded by FFREE) never refill a slot that is still unread
+constexpr int kStatSlots = 3;
+constexpr int kOffStat = kOffFine + 8 * kFineWarp;
+constexpr int kOffEnt = kOffStat + kStatSlots * 2 * kTileQ * 4;  // bias[32], chunk info[8], rows[32]
 constexpr int kOffBar = kOffEnt + 256;
 enum { QFULL = 0, QEMPTY = 2, KFULL = 4, KEMPTY = 7, SREADY = 10, TFREE = 12, DSREADY = 14,
-       DSFREE = 16, DQREADY = 18, DQFREE = 20, DREADY = 22, FDONE = 24, FFREE = 26,
-       STATFREE = 28, NBAR = 30 };
+       DSFREE = 16, DQREADY = 18, DQFREE = 20, FDONE = 22, FFREE = 24, DREADY = 26,
+       NBAR = 29 };
 constexpr int kSmem = kOffBar + NBAR * 8 + 16;
 static_assert(kSmem <= 232448, "dqf shared memory over the 227 KB opt-in limit");
 constexpr int kThreads = 16 * 32;
@@ -2454,7 +2457,7 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   auto bar = [&](int i) { return sbase + kOffBar + 8u * i; };
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + kOffBar + NBAR * 8);
-  float* stat = reinterpret_cast<float*>(smem + kOffStat);  // [2 tiles][lse | D][128]
+  float* stat = reinterpret_cast<float*>(smem + kOffStat);  // [3 tiles][lse | D][128]
   float* ent_bias = reinterpret_cast<float*>(smem + kOffEnt);
   uint32_t* ch_info = reinterpret_cast<uint32_t*>(smem + kOffEnt + 128);
   const uint64_t tpu = p.n / kTileQ;
@@ -2484,9 +2487,9 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       mbar_init(bar(DSFREE + i), 1);
       mbar_init(bar(DQREADY + i), 1);
       mbar_init(bar(DQFREE + i), 128);
-      mbar_init(bar(DREADY + i), 256);
-      mbar_init(bar(STATFREE + i), 128);  // the coarse warps hold tile i's LSE / D
+
     }
+    for (int i = 0; i < kStatSlots; ++i) mbar_init(bar(DREADY + i), 256);
     fence_mbar_init();
   }
   fence_before();
@@ -2628,13 +2631,10 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       const uint64_t q0 = (id % tpu) * kTileQ;
       const uint32_t tb = i & 1;
       if (tid == 96) trace_ev(p, 7, i, 5);
-      mbar_wait(bar(DREADY + tb), (i >> 1) & 1);
+      const uint32_t ts = i % kStatSlots;
+      mbar_wait(bar(DREADY + ts), (i / kStatSlots) & 1);
       if (tid == 96) trace_ev(p, 7, i, 6);
-      const float lse = stat[tb * 256 + row], Drow = stat[tb * 256 + 128 + row];
-      // the fine warps may overwrite stat[tb] with tile i+2's values only
-      // after this (they can be two tiles ahead of this point: nothing else
-      // orders their tile i+2 start after this read)
-      mbar_arrive(bar(STATFREE + tb));
+      const float lse = stat[ts * 256 + row], Drow = stat[ts * 256 + 128 + row];
       for (uint32_t ch = 0; ch < nch; ++ch, ++c) {
         const uint32_t b = c & 1, ne = ch_info[ch] & 0xFF;
         if (tid == 96) trace_ev(p, 4, c, 1);
@@ -2849,15 +2849,14 @@ __global__ void __launch_bounds__(dqf::kThreads, 1)
       }
       __syncwarp();  // the Q/dO stage is overwritten by fine block kFS-1
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
-      const uint32_t tb = i & 1;
-      if (i >= 2) mbar_wait(bar(STATFREE + tb), ((i >> 1) - 1) & 1);
+      const uint32_t tb = i & 1, ts = i % kStatSlots;
       if (half == 0) {
         p.drow[ro + trow] = dsum;
         p.lse2[ro + trow] = lse_r;
-        stat[tb * 256 + fw * 16 + rr] = lse_r;
-        stat[tb * 256 + 128 + fw * 16 + rr] = dsum;
+        stat[ts * 256 + fw * 16 + rr] = lse_r;
+        stat[ts * 256 + 128 + fw * 16 + rr] = dsum;
       }
-      mbar_arrive(bar(DREADY + tb));
+      mbar_arrive(bar(DREADY + ts));
       if (tid == 224) trace_ev(p, 5, i, 3);
       const float D0 = __shfl_sync(0xffffffffu, dsum, 2 * r);
       const float D1 = __shfl_sync(0xffffffffu, dsum, 2 * (r + 8));

@@ -98,12 +98,10 @@ g_arr = ln("if (lane == 0) mbar_arrive(bar(FACTE + fs));", k0)
 e_wait = ln("mbar_wait(bar(FACTF + fs), (it / kFactSlots) & 1);", g_wait)
 e_arr = ln("if (lane == 0) mbar_arrive(bar(FACTE + fs));", g_arr)
 d0 = ln("tc5_dqf_kernel(const __grid_constant__")
-d_wait = ln("mbar_wait(bar(DREADY + tb), (i >> 1) & 1);", d0)
-d_read = ln("const float lse = stat[tb * 256 + row], Drow", d0)
-d_free = ln("mbar_arrive(bar(STATFREE + tb));", d0)
-d_fw = ln("mbar_wait(bar(STATFREE + tb)", d0)
-d_w1 = ln("stat[tb * 256 + fw * 16 + rr] = lse_r;", d0)
-d_arr = ln("mbar_arrive(bar(DREADY + tb));", d0)
+d_wait = ln("mbar_wait(bar(DREADY + ts), (i / kStatSlots) & 1);", d0)
+d_read = ln("const float lse = stat[ts * 256 + row], Drow", d0)
+d_w1 = ln("stat[ts * 256 + fw * 16 + rr] = lse_r;", d0)
+d_arr = ln("mbar_arrive(bar(DREADY + ts));", d0)
 prose = (
     f"* `tc5_kvf_kernel` `attn_tc.cu:{r_lo}/{r_ids}` (the gather warps read the item-facts "
     f"ring) vs `:{w_kb}/{w_qb}` (the facts warp writes it): the writer waits `FACTE[slot]` "
@@ -112,14 +110,13 @@ prose = (
     f"in registers (`:{g_arr}`, `:{e_arr}`), and wait `FACTF[slot]` (`:{g_wait}`, "
     f"`:{e_wait}`), which the writer arrives after its stores (`:{w_arr}`). A full/empty "
     f"ring.\n"
-    f"* `tc5_dqf_kernel` `attn_tc.cu:{d_read}` (coarse warps read the tile's LSE / D from "
-    f"`stat[tb]`) vs `:{d_w1}-{d_w1 + 1}` (fine warps write `stat[tb]` for tile i+2): the "
-    f"reads follow `DREADY[tb]` (`:{d_wait}`, arrived at `:{d_arr}`), and the coarse warps "
-    f"arrive on `STATFREE[tb]` right after reading (`:{d_free}`), which the fine warps wait "
-    f"for before refilling the slot (`:{d_fw}`).  This pair was a real race until round 2's "
-    f"`STATFREE` barrier (the refill had no ordering after the read; a 128-unit batch showed "
-    f"garbage dq in a few units — DESIGN §4); with the barrier in place racecheck no longer "
-    f"reports it.\n\n")
+    f"* `tc5_dqf_kernel` `attn_tc.cu:{d_read}` (coarse warps read the tile's LSE / D) vs "
+    f"`:{d_w1}-{d_w1 + 1}` (fine warps write them for a later tile): until round 2 this "
+    f"two-slot ring had no ordering of the refill after the read — a real race (a 128-unit "
+    f"batch showed garbage dq in a few units, DESIGN §4).  The ring now has three slots "
+    f"(`DREADY`, `:{d_wait}` / `:{d_arr}`); the fine warps, at most two tiles ahead "
+    f"(bounded by `FFREE`), never refill an unread slot, and racecheck no longer reports "
+    f"the pair.\n\n")
 i = sd.index("* `tc5_kvf_kernel` `attn_tc.cu:")
 j = sd.index("memcheck and synccheck: 0 errors")
 sd = sd[:i] + prose + sd[j:]
